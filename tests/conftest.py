@@ -1,0 +1,46 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    config.addinivalue_line("markers", "slow: long-running (still part of the suite)")
+
+
+def load_golden(name="worked_values.txt"):
+    out = {}
+    with open(os.path.join(ROOT, "tests", "golden", name)) as fh:
+        for line in fh:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            key, vals, cite = [s.strip() for s in line.split("|", 2)]
+            out[key] = (np.array([float(v) for v in vals.split()]), cite)
+    return out
+
+
+def load_markov_golden():
+    mats, cur = {}, None
+    with open(os.path.join(ROOT, "tests", "golden", "markov_matrices.txt")) as fh:
+        for line in fh:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            if line[0].isalpha() or line[0].isdigit() and "." not in line:
+                cur = line
+                mats[cur] = []
+            else:
+                mats[cur].append([float(v) for v in line.split()])
+    return {k: np.array(v) for k, v in mats.items()}
+
+
+@pytest.fixture(scope="session")
+def golden():
+    return load_golden()
