@@ -1,0 +1,184 @@
+/*
+ * gfq.h -- C ABI of libgfq: batched belief-propagation decoding of
+ * MacKay-Neal codes over GF(2^p) (q = 2^p = 2..64) on one NVIDIA B200.
+ *
+ * Method: Yacov, Efraim, Kfir, Kanter, Shental, "Parallel vs. Sequential
+ * Belief Propagation Decoding of LDPC Codes over GF(q) and Markov Sources"
+ * (PAPER.md; cited P:line).  The decoder is given the code H = [A B]
+ * (P:121-126), a batch of received frames and the prior knowledge
+ * of source and channel, and recovers x = [s; n] from the syndrome z = B r
+ * (Eq. 2) by BP with the parallel (PUS) or sequential
+ * (SUS) updating scheme, with dynamical Markov block priors
+ * (Eqs. 6/7) for correlated sources.
+ *
+ * Conventions (all calls):
+ *   - Return 0 (GFQ_OK) or a negative GFQ_E* code; no exception crosses the
+ *     ABI.  gfq_last_error() returns a thread-local message for the last failure.
+ *   - GF(2^p) symbols are bytes; element a has polynomial-basis bits LSB first,
+ *     bit b of symbol k is transmitted bit k*p + b (reading A2).
+ *   - "device" pointers are CUDA device memory on the current device; "host"
+ *     pointers are ordinary (pageable or pinned) host memory.
+ *   - Every decode call is asynchronous on `stream` (a cudaStream_t passed as
+ *     void*, NULL = legacy default stream) unless documented otherwise; its
+ *     outputs are valid once that stream has been synchronised.
+ *   - The library owns only the code object.  All per-decode buffers (inputs,
+ *     outputs, workspace) are allocated and owned by the caller; the decode
+ *     path never calls cudaMalloc.
+ *   - Decoding is deterministic: identical inputs on the same GPU give
+ *     identical outputs.
+ *   - There is no CPU fallback: without a usable CUDA device every decode call
+ *     fails with GFQ_ECUDA.
+ */
+#ifndef GFQ_H
+#define GFQ_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GFQ_OK 0
+#define GFQ_EINVAL (-1)       /* bad argument (see each call)                  */
+#define GFQ_ENOMEM (-2)       /* host or device allocation failed (create only) */
+#define GFQ_ECUDA (-3)        /* CUDA runtime error (message has the details)   */
+#define GFQ_EUNSUPPORTED (-4) /* valid but not implemented (p > 6, degree > 8)   */
+
+typedef enum { GFQ_BSC = 0, GFQ_BEC = 1, GFQ_BIAWGN = 2 } gfq_channel;
+typedef enum { GFQ_PUS = 0, GFQ_SUS = 1 } gfq_schedule;
+
+/* Opaque, immutable after creation; may be shared by concurrent decodes on
+ * different streams (each with its own workspace). */
+typedef struct gfq_code gfq_code;
+
+typedef struct {
+    /* Channel of the received bits:
+     *   GFQ_BSC:    ch_param = flip probability f, 0 < f < 1/2.
+     *   GFQ_BEC:    ch_param = erasure probability (informational; an erased
+     *               bit carries no evidence: likelihood 1/2 each, reading A15).
+     *   GFQ_BIAWGN: ch_param = noise standard deviation sigma > 0 for
+     *               unit-energy BPSK 0 -> +1, 1 -> -1 (reading A16). */
+    int channel;
+    double ch_param;
+    int schedule;      /* GFQ_PUS or GFQ_SUS          */
+    int max_iters;     /* >= 0; 0 returns iters = -1 and the clipped priors    */
+    int early_exit;    /* 1: a frame stops at the first iteration t with
+                          H x = z; 0: every frame runs exactly
+                          max_iters iterations (throughput / parity mode) and
+                          still reports the first passing t.                  */
+    const double *markov_T; /* host, q*q row-stochastic T[a*q+b] = Pr(b | a),
+                               the "measured Markov transition matrix"
+                               (reading A13), or NULL = i.i.d.     */
+    const double *src_pi0;  /* host, q: prior of the first source symbol and of
+                               every source symbol for i.i.d. sources
+                               (P:224-226); NULL = uniform 1/q.               */
+    int keep_messages; /* 1: keep the final q, r messages and all posteriors Q
+                          in the workspace for gfq_export_messages (needs a
+                          workspace sized with the same flag).                */
+} gfq_params;
+
+/* Thread-local description of the last error (never NULL). */
+const char *gfq_last_error(void);
+
+/* ABI version: 0x010000 * major + 0x100 * minor + patch. */
+int gfq_version(void);
+
+/* Build a code object from the two sparse matrices of the MN code
+ * (P:121-126): A is M x N, B is M x M, both in host COO form with 0-based
+ * (row, col) and GF(2^p) values in 1..q-1.  H = [A B] (Eq. 2): check i is
+ * row i; variable j < N is source symbol s_j, variable N + k is noise symbol
+ * n_k (B column k).  prim_poly is the primitive polynomial of GF(2^p) with
+ * the x^p term (e.g. 0x43 = x^6+x+1).  The host arrays are copied; the
+ * device tables (check-major and variable-major edge maps, coefficient
+ * permutations, SUS dependency levels) are uploaded to the current device.
+ * B's invertibility is NOT checked: decoding needs only H and z; it matters
+ * to the encoder (Eq. 1) only.
+ * Errors: GFQ_EINVAL for p < 1, N < 0, M < 1, a polynomial that is not
+ * primitive of degree p, an index out of range, a value 0 or >= q, or a
+ * duplicate (row, col); GFQ_EUNSUPPORTED for p > 6 or a check/variable degree
+ * > 8; GFQ_ENOMEM / GFQ_ECUDA from allocation or upload.  *out is set only on
+ * success. */
+int gfq_code_create(gfq_code **out, int p, unsigned prim_poly, int N, int M,
+                    long long nnzA, const int *A_row, const int *A_col,
+                    const unsigned char *A_val, long long nnzB, const int *B_row,
+                    const int *B_col, const unsigned char *B_val);
+
+/* Release a code object (NULL is a no-op).  No decode may be in flight. */
+void gfq_code_destroy(gfq_code *code);
+
+/* Sizes of the Tanner graph: E = nnz(H), maximum check / variable degree, and
+ * the number of SUS dependency levels (columns sharing no check commute; the
+ * sequential sweep executes level by level).  NULL outputs are
+ * skipped. */
+int gfq_code_info(const gfq_code *code, long long *n_edges, int *max_check_deg,
+                  int *max_var_deg, int *sus_levels);
+
+/* Bytes of device workspace that decode n_frames frames in ONE wave with these
+ * params.  A smaller workspace (but at least gfq_workspace_bytes(code, 1, p))
+ * is accepted by the decode calls, which then process the frames in waves of
+ * as many 32-frame blocks as fit.  Returns 0 on bad arguments. */
+size_t gfq_workspace_bytes(const gfq_code *code, int n_frames, const gfq_params *params);
+
+/* Decode a batch from channel outputs (device pointers):
+ *   obs:   GFQ_BSC    uint8 [n_frames][M*p] received bits 0/1;
+ *          GFQ_BEC    uint8 [n_frames][M*p] 0/1, or 2 = erased;
+ *          GFQ_BIAWGN float [n_frames][M*p] received values y.
+ *   s_hat: uint8 [n_frames][N] out: decoded source symbols (clipped
+ *          pseudo-posterior) at the iteration reported in iters,
+ *          or at the last iteration if the frame never converged.
+ *   iters: int32 [n_frames] out: first t in 1..max_iters with H x = z
+ *          (P:190-194), or -1 if none (reading A21).
+ *   workspace / ws_bytes: device scratch (>= gfq_workspace_bytes(code, 1, p)).
+ * Errors: GFQ_EINVAL for NULL code/params/pointers, n_frames < 0, bad
+ * channel/schedule, max_iters < 0, a markov_T row not stochastic, ws_bytes too
+ * small, or keep_messages with a workspace that cannot hold all frames;
+ * GFQ_ECUDA on a launch failure (no device, bad pointer). */
+int gfq_decode(const gfq_code *code, int n_frames, const void *obs,
+               const gfq_params *params, unsigned char *s_hat, int *iters,
+               void *workspace, size_t ws_bytes, void *stream);
+
+/* Lower-level entry with the channel front end supplied by the caller
+ * (device pointers): hard_bits uint8 [n_frames][M*p] hard decisions r_b and
+ * bit_flip_prob float [n_frames][M*p] the probability pi_b that noise bit n_b
+ * is 1 (r = t + n mod 2).  params->channel/ch_param are ignored.
+ * x_hat: uint8 [n_frames][N+M] out: the whole estimate x = [s; n]. */
+int gfq_decode_evidence(const gfq_code *code, int n_frames, const unsigned char *hard_bits,
+                        const float *bit_flip_prob, const gfq_params *params,
+                        unsigned char *x_hat, int *iters, void *workspace,
+                        size_t ws_bytes, void *stream);
+
+/* End-to-end entry with HOST buffers: obs (layout as gfq_decode) is copied to
+ * the device, decoded, and s_hat / iters are copied back; the call returns
+ * after synchronising `stream`.  The workspace must be large enough to hold
+ * the device copy of obs in addition to gfq_workspace_bytes for one wave:
+ * size it with gfq_workspace_bytes_host. */
+size_t gfq_workspace_bytes_host(const gfq_code *code, int n_frames, const gfq_params *params);
+int gfq_decode_host(const gfq_code *code, int n_frames, const void *obs_host,
+                    const gfq_params *params, unsigned char *s_hat_host, int *iters_host,
+                    void *workspace, size_t ws_bytes, void *stream);
+
+/* Export the messages left in the workspace by the last decode made with
+ * keep_messages = 1 (all frames in one wave), in the probability domain and
+ * canonical edge order (column-major: j ascending, then i ascending), all
+ * device pointers, NULL to skip:
+ *   q_msg [n_frames][E][q]  q_ij^a after the last iteration (Eq. 4),
+ *   r_msg [n_frames][E][q]  r_ij^a last computed (Eq. 3; SUS: in the last sweep),
+ *   Q     [n_frames][N+M][q] pseudo-posteriors of the last iteration (Eq. 5).
+ * For frames that stopped early (early_exit = 1) the values are those of the
+ * iteration in which their 32-frame block stopped.  Errors: GFQ_EINVAL. */
+int gfq_export_messages(const gfq_code *code, int n_frames, const void *workspace,
+                        size_t ws_bytes, const gfq_params *params, float *q_msg,
+                        float *r_msg, float *Q, void *stream);
+
+/* Health counters of the last decode that used this workspace (host out,
+ * synchronises `stream`): stats[0] vanished or non-finite normalisers replaced
+ * by a uniform vector (reading A19; 0 on parity runs), stats[1] iterations
+ * executed summed over 32-frame blocks, stats[2] frames converged, stats[3]
+ * kernel launches issued by the decode. */
+int gfq_decode_stats(const gfq_code *code, const void *workspace, size_t ws_bytes,
+                     long long stats[4], void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GFQ_H */

@@ -1,0 +1,242 @@
+// gfq_code.cu -- code object: validation, Tanner-graph maps, GF(2^p) tables,
+// SUS dependency levels, upload.  Host C++ (runs once per code).
+//
+// H = [A B]: check i = row i, variable j < N = source
+// symbol s_j, variable N + k = noise symbol n_k.  "The non-zero elements in a
+// row i of H represent the [symbols] of x participating in check z_i; the
+// non-zero elements in column j represent the checks in which the j'th
+// [symbol] participates".
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "gfq_internal.cuh"
+
+namespace gfq {
+
+static thread_local std::string g_err = "no error";
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+int cuda_fail(cudaError_t e, const char *what) {
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return GFQ_ECUDA;
+}
+
+// GF(2^p) log/antilog tables (the library's own; the oracle multiplies by
+// shift-and-xor and the input generator has a third implementation).
+struct GF {
+  int p, q;
+  std::vector<int> exp, log;
+  bool build(int p_, unsigned poly) {
+    p = p_;
+    q = 1 << p;
+    exp.assign(2 * q, 0);
+    log.assign(q, -1);
+    int a = 1;
+    for (int k = 0; k < q - 1; ++k) {
+      if (log[a] != -1) return false;  // x is not a generator -> not primitive
+      exp[k] = a;
+      log[a] = k;
+      a <<= 1;
+      if (a & q) a ^= (int)poly;
+      if (a >= q || a == 0) return false;
+    }
+    if (a != 1) return false;
+    for (int k = q - 1; k < 2 * q; ++k) exp[k] = exp[k % (q - 1)];
+    return true;
+  }
+  int mul(int x, int y) const { return (x && y) ? exp[log[x] + log[y]] : 0; }
+  int inv(int x) const { return exp[(q - 1 - log[x]) % (q - 1)]; }
+};
+
+}  // namespace gfq
+
+using namespace gfq;
+
+extern "C" const char *gfq_last_error(void) { return g_err.c_str(); }
+
+extern "C" int gfq_version(void) { return 0x010000; }
+
+extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int M,
+                               long long nnzA, const int *A_row, const int *A_col,
+                               const unsigned char *A_val, long long nnzB,
+                               const int *B_row, const int *B_col,
+                               const unsigned char *B_val) {
+  if (!out) { set_error("gfq_code_create: out is NULL"); return GFQ_EINVAL; }
+  if (p > 6) { set_error("gfq_code_create: p > 6 unsupported"); return GFQ_EUNSUPPORTED; }
+  if (p < 1 || N < 0 || M < 1 || nnzA < 0 || nnzB < 0) {
+    set_error("gfq_code_create: bad sizes");
+    return GFQ_EINVAL;
+  }
+  if ((nnzA && (!A_row || !A_col || !A_val)) || (nnzB && (!B_row || !B_col || !B_val))) {
+    set_error("gfq_code_create: NULL COO array");
+    return GFQ_EINVAL;
+  }
+  if (poly >> p != 1u) { set_error("gfq_code_create: polynomial degree != p"); return GFQ_EINVAL; }
+  GF gf;
+  if (!gf.build(p, poly)) { set_error("gfq_code_create: polynomial is not primitive"); return GFQ_EINVAL; }
+  const int q = 1 << p, V = N + M;
+  const long long E = nnzA + nnzB;
+  if (E > (1LL << 31) - 1) { set_error("gfq_code_create: too many edges"); return GFQ_EUNSUPPORTED; }
+
+  struct Ent { int r, c, v; };
+  std::vector<Ent> ent((size_t)E);
+  for (long long k = 0; k < nnzA; ++k) {
+    if (A_row[k] < 0 || A_row[k] >= M || A_col[k] < 0 || A_col[k] >= N) {
+      set_error("gfq_code_create: A index out of range");
+      return GFQ_EINVAL;
+    }
+    if (A_val[k] == 0 || A_val[k] >= q) { set_error("gfq_code_create: A value not in 1..q-1"); return GFQ_EINVAL; }
+    ent[k] = {A_row[k], A_col[k], A_val[k]};
+  }
+  for (long long k = 0; k < nnzB; ++k) {
+    if (B_row[k] < 0 || B_row[k] >= M || B_col[k] < 0 || B_col[k] >= M) {
+      set_error("gfq_code_create: B index out of range");
+      return GFQ_EINVAL;
+    }
+    if (B_val[k] == 0 || B_val[k] >= q) { set_error("gfq_code_create: B value not in 1..q-1"); return GFQ_EINVAL; }
+    ent[nnzA + k] = {B_row[k], N + B_col[k], B_val[k]};
+  }
+  std::sort(ent.begin(), ent.end(), [](const Ent &a, const Ent &b) {
+    return a.r != b.r ? a.r < b.r : a.c < b.c;
+  });
+  for (long long k = 1; k < E; ++k)
+    if (ent[k].r == ent[k - 1].r && ent[k].c == ent[k - 1].c) {
+      set_error("gfq_code_create: duplicate (row, col)");
+      return GFQ_EINVAL;
+    }
+
+  // check-major edge ids (CSR order)
+  std::vector<int> row_ptr(M + 1, 0), edge_var(E), edge_check(E), col_ptr(V + 1, 0), col_edge(E);
+  std::vector<unsigned char> edge_coef(E);
+  std::vector<unsigned long long> edge_perm(E);
+  for (long long e = 0; e < E; ++e) {
+    row_ptr[ent[e].r + 1]++;
+    col_ptr[ent[e].c + 1]++;
+    edge_var[e] = ent[e].c;
+    edge_check[e] = ent[e].r;
+    edge_coef[e] = (unsigned char)ent[e].v;
+    const int hinv = gf.inv(ent[e].v);
+    unsigned long long pk = 0;
+    for (int b = 0; b < p; ++b) pk |= (unsigned long long)gf.mul(hinv, 1 << b) << (8 * b);
+    edge_perm[e] = pk;
+  }
+  for (int i = 0; i < M; ++i) row_ptr[i + 1] += row_ptr[i];
+  for (int j = 0; j < V; ++j) col_ptr[j + 1] += col_ptr[j];
+  {
+    std::vector<int> fill(col_ptr.begin(), col_ptr.end() - 1);
+    for (long long e = 0; e < E; ++e) col_edge[fill[edge_var[e]]++] = (int)e;  // ascending check
+  }
+  int max_cdeg = 0, max_vdeg = 0;
+  for (int i = 0; i < M; ++i) max_cdeg = std::max(max_cdeg, row_ptr[i + 1] - row_ptr[i]);
+  for (int j = 0; j < V; ++j) max_vdeg = std::max(max_vdeg, col_ptr[j + 1] - col_ptr[j]);
+  if (max_cdeg > kMaxDeg || max_vdeg > kMaxDeg) {
+    set_error("gfq_code_create: a check or variable degree exceeds 8");
+    return GFQ_EUNSUPPORTED;
+  }
+
+  // SUS dependency levels: in the
+  // sweep j = 0..V-1 (order A7) column j reads the q's of the other
+  // columns of its checks.  level(j) = 1 + max level of the earlier columns
+  // sharing a check with j; columns of one level share no check, so running a
+  // level's columns concurrently, levels in order, reads exactly the values
+  // the serial sweep reads.
+  std::vector<int> lvl(V, 0), rowlvl(M, 0);
+  int nlev = 0;
+  for (int j = 0; j < V; ++j) {
+    int L = 0;
+    for (int k = col_ptr[j]; k < col_ptr[j + 1]; ++k) L = std::max(L, rowlvl[edge_check[col_edge[k]]]);
+    L += 1;
+    lvl[j] = L;
+    for (int k = col_ptr[j]; k < col_ptr[j + 1]; ++k) rowlvl[edge_check[col_edge[k]]] = L;
+    nlev = std::max(nlev, L);
+  }
+  std::vector<int> level_ptr(nlev + 1, 0), level_cols(V);
+  for (int j = 0; j < V; ++j) level_ptr[lvl[j]]++;      // lvl in 1..nlev -> slot lvl
+  for (int L = 0; L < nlev; ++L) level_ptr[L + 1] += level_ptr[L];
+  {
+    std::vector<int> fill(level_ptr.begin(), level_ptr.end() - 1);
+    for (int j = 0; j < V; ++j) level_cols[fill[lvl[j] - 1]++] = j;
+  }
+
+  std::vector<unsigned char> mul((size_t)q * q);
+  for (int x = 0; x < q; ++x)
+    for (int y = 0; y < q; ++y) mul[x * q + y] = (unsigned char)gf.mul(x, y);
+
+  // one device blob
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  size_t off = 0;
+  const size_t o_row = off; off += al(sizeof(int) * (M + 1));
+  const size_t o_var = off; off += al(sizeof(int) * E);
+  const size_t o_chk = off; off += al(sizeof(int) * E);
+  const size_t o_perm = off; off += al(sizeof(unsigned long long) * E);
+  const size_t o_coef = off; off += al(E);
+  const size_t o_col = off; off += al(sizeof(int) * (V + 1));
+  const size_t o_cedge = off; off += al(sizeof(int) * E);
+  const size_t o_lptr = off; off += al(sizeof(int) * (nlev + 1));
+  const size_t o_lcol = off; off += al(sizeof(int) * V);
+  const size_t o_mul = off; off += al((size_t)q * q);
+  std::vector<unsigned char> host(off, 0);
+  auto put = [&](size_t o, const void *src, size_t n) { if (n) memcpy(host.data() + o, src, n); };
+  put(o_row, row_ptr.data(), sizeof(int) * (M + 1));
+  put(o_var, edge_var.data(), sizeof(int) * E);
+  put(o_chk, edge_check.data(), sizeof(int) * E);
+  put(o_perm, edge_perm.data(), sizeof(unsigned long long) * E);
+  put(o_coef, edge_coef.data(), E);
+  put(o_col, col_ptr.data(), sizeof(int) * (V + 1));
+  put(o_cedge, col_edge.data(), sizeof(int) * E);
+  put(o_lptr, level_ptr.data(), sizeof(int) * (nlev + 1));
+  put(o_lcol, level_cols.data(), sizeof(int) * V);
+  put(o_mul, mul.data(), (size_t)q * q);
+
+  int dev = 0;
+  cudaError_t ce = cudaGetDevice(&dev);
+  if (ce != cudaSuccess) return cuda_fail(ce, "gfq_code_create: cudaGetDevice");
+  void *blob = nullptr;
+  ce = cudaMalloc(&blob, off);
+  if (ce != cudaSuccess) { cudaGetLastError(); set_error("gfq_code_create: cudaMalloc failed"); return GFQ_ENOMEM; }
+  ce = cudaMemcpy(blob, host.data(), off, cudaMemcpyHostToDevice);
+  if (ce != cudaSuccess) { cudaFree(blob); return cuda_fail(ce, "gfq_code_create: upload"); }
+
+  gfq_code *c = new (std::nothrow) gfq_code();
+  if (!c) { cudaFree(blob); set_error("gfq_code_create: out of host memory"); return GFQ_ENOMEM; }
+  c->p = p; c->q = q; c->N = N; c->M = M; c->V = V; c->poly = poly; c->E = E;
+  c->max_cdeg = max_cdeg; c->max_vdeg = max_vdeg; c->n_levels = nlev; c->device = dev;
+  c->level_ptr_h = level_ptr;
+  c->dev_blob = blob;
+  unsigned char *b = (unsigned char *)blob;
+  c->d.p = p; c->d.q = q; c->d.N = N; c->d.M = M; c->d.V = V; c->d.E = E;
+  c->d.max_cdeg = max_cdeg; c->d.max_vdeg = max_vdeg;
+  c->d.row_ptr = (const int *)(b + o_row);
+  c->d.edge_var = (const int *)(b + o_var);
+  c->d.edge_check = (const int *)(b + o_chk);
+  c->d.edge_perm = (const unsigned long long *)(b + o_perm);
+  c->d.edge_coef = b + o_coef;
+  c->d.col_ptr = (const int *)(b + o_col);
+  c->d.col_edge = (const int *)(b + o_cedge);
+  c->d.level_ptr = (const int *)(b + o_lptr);
+  c->d.level_cols = (const int *)(b + o_lcol);
+  c->d.mul = b + o_mul;
+  *out = c;
+  return GFQ_OK;
+}
+
+extern "C" void gfq_code_destroy(gfq_code *c) {
+  if (!c) return;
+  if (c->dev_blob) cudaFree(c->dev_blob);
+  delete c;
+}
+
+extern "C" int gfq_code_info(const gfq_code *c, long long *n_edges, int *max_check_deg,
+                             int *max_var_deg, int *sus_levels) {
+  if (!c) { set_error("gfq_code_info: code is NULL"); return GFQ_EINVAL; }
+  if (n_edges) *n_edges = c->E;
+  if (max_check_deg) *max_check_deg = c->max_cdeg;
+  if (max_var_deg) *max_var_deg = c->max_vdeg;
+  if (sus_levels) *sus_levels = c->n_levels;
+  return GFQ_OK;
+}

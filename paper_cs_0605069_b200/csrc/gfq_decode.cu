@@ -1,0 +1,363 @@
+// gfq_decode.cu -- decode driver: workspace layout, waves over 32-frame
+// blocks, the BP iteration loop (PUS or SUS), convergence bookkeeping,
+// message export and health counters.  Host C++; every arithmetic step runs
+// in the kernels of gfq_kernels.cu.
+//
+// One iteration:
+//   PUS: k_cn (horizontal pass, Eq. 3) -> k_vn (vertical pass Eq. 4 +
+//        posterior Eq. 5 + clipping; Markov prior Eq. 7 fused)
+//   SUS: k_sus once per dependency level (steps 1-4 for every column)
+//   then k_test (H x = z per frame) -> k_finalize -> k_capture
+//   (copy x of newly converged frames) -> k_compact (early exit: drop
+//   32-frame blocks whose frames all converged).
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "gfq_internal.cuh"
+
+namespace gfq {
+
+static inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+static constexpr size_t kNone = (size_t)-1;
+
+Layout make_layout(const gfq_code *c, int fbw, const gfq_params *prm) {
+  Layout L;
+  L.fbw = fbw;
+  size_t off = 0;
+  const size_t F32 = (size_t)fbw * 32;
+  const size_t Mp = (size_t)c->M * c->p;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += al256(bytes);
+    return o;
+  };
+  // fixed header at offset 0 (gfq_decode_stats reads it without the params)
+  L.stats = take(4 * sizeof(unsigned long long));
+  L.nactive = take(sizeof(int));
+  L.T = take((size_t)c->q * c->q * sizeof(double));
+  L.pi0 = take((size_t)c->q * sizeof(double));
+  const size_t msg = (size_t)c->E * c->q * F32 * sizeof(float);
+  L.qmsg = take(msg);
+  const bool need_r = prm->schedule == GFQ_PUS || prm->keep_messages;
+  L.rmsg = need_r ? take(msg) : kNone;
+  L.pi = take(Mp * F32 * sizeof(float));
+  L.hard = take(Mp * F32);
+  L.z = take((size_t)c->M * F32);
+  L.xhat = take((size_t)c->V * F32);
+  const bool markov = prm->markov_T != nullptr;
+  const size_t qs = (size_t)c->N * c->q * F32 * sizeof(float);
+  L.qs0 = markov ? take(qs) : kNone;
+  L.qs1 = markov ? take(qs) : kNone;
+  L.qall = prm->keep_messages ? take((size_t)c->V * c->q * F32 * sizeof(float)) : kNone;
+  L.iters = take(F32 * sizeof(int));
+  L.conv = take(F32 * sizeof(int));
+  L.unsat = take(F32 * sizeof(int));
+  L.newconv = take(F32 * sizeof(int));
+  L.active = take((size_t)fbw * sizeof(int));
+  L.list = take((size_t)fbw * sizeof(int));
+  L.total = off;
+  return L;
+}
+
+static int check_params(const gfq_code *c, const gfq_params *prm, bool need_channel) {
+  if (!c) { set_error("code is NULL"); return GFQ_EINVAL; }
+  if (!prm) { set_error("params is NULL"); return GFQ_EINVAL; }
+  if (prm->schedule != GFQ_PUS && prm->schedule != GFQ_SUS) { set_error("bad schedule"); return GFQ_EINVAL; }
+  if (prm->max_iters < 0) { set_error("max_iters < 0"); return GFQ_EINVAL; }
+  if (need_channel) {
+    if (prm->channel < GFQ_BSC || prm->channel > GFQ_BIAWGN) { set_error("bad channel"); return GFQ_EINVAL; }
+    if (prm->channel == GFQ_BSC && !(prm->ch_param >= 0.0 && prm->ch_param <= 1.0)) {
+      set_error("BSC flip probability must be in [0, 1]");
+      return GFQ_EINVAL;
+    }
+    if (prm->channel == GFQ_BIAWGN && !(prm->ch_param > 0.0)) { set_error("BI-AWGN sigma must be > 0"); return GFQ_EINVAL; }
+  }
+  const int q = c->q;
+  if (prm->markov_T) {
+    for (int a = 0; a < q; ++a) {
+      double s = 0.0;
+      for (int b = 0; b < q; ++b) {
+        const double v = prm->markov_T[a * q + b];
+        if (!(v >= 0.0) || !std::isfinite(v)) { set_error("markov_T has a negative or non-finite entry"); return GFQ_EINVAL; }
+        s += v;
+      }
+      if (std::fabs(s - 1.0) > 1e-6) { set_error("markov_T row is not stochastic"); return GFQ_EINVAL; }
+    }
+  }
+  if (prm->src_pi0) {
+    double s = 0.0;
+    for (int a = 0; a < q; ++a) {
+      if (!(prm->src_pi0[a] >= 0.0)) { set_error("src_pi0 has a negative entry"); return GFQ_EINVAL; }
+      s += prm->src_pi0[a];
+    }
+    if (std::fabs(s - 1.0) > 1e-6) { set_error("src_pi0 does not sum to 1"); return GFQ_EINVAL; }
+  }
+  return GFQ_OK;
+}
+
+// Largest number of 32-frame blocks per wave that fits ws_bytes (<= want).
+static int blocks_fitting(const gfq_code *c, const gfq_params *prm, size_t ws_bytes, int want) {
+  if (want <= 0) return 0;
+  if (make_layout(c, want, prm).total <= ws_bytes) return want;
+  int lo = 0, hi = want;  // lo fits (0 trivially), hi does not
+  while (hi - lo > 1) {
+    const int mid = lo + (hi - lo) / 2;
+    if (make_layout(c, mid, prm).total <= ws_bytes) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+template <typename T>
+static T *at(void *ws, size_t off) {
+  return off == kNone ? nullptr : (T *)((char *)ws + off);
+}
+
+struct LagRing {
+  static constexpr int K = 8;
+  cudaEvent_t ev[K];
+  unsigned *host = nullptr;
+  bool ok = false;
+  LagRing() {
+    if (cudaMallocHost((void **)&host, K * sizeof(unsigned)) != cudaSuccess) { cudaGetLastError(); return; }
+    for (int k = 0; k < K; ++k)
+      if (cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming) != cudaSuccess) { cudaGetLastError(); return; }
+    ok = true;
+  }
+};
+
+static LagRing &lag_ring() {
+  static thread_local LagRing r;
+  return r;
+}
+
+// mode: 0 BSC, 1 BEC, 2 BI-AWGN (obs), 3 evidence (hard_in + pi_in)
+static int decode_common(const gfq_code *c, int F, int mode, double ch_param, const void *obs,
+                         const unsigned char *hard_in, const float *pi_in, const gfq_params *prm,
+                         unsigned char *out, int Lout, int *iters_out, void *ws, size_t ws_bytes,
+                         cudaStream_t st) {
+  if (F < 0) { set_error("n_frames < 0"); return GFQ_EINVAL; }
+  if (F == 0) return GFQ_OK;
+  if (!ws || !out || !iters_out || (mode < 3 && !obs) || (mode == 3 && (!hard_in || !pi_in))) {
+    set_error("NULL buffer");
+    return GFQ_EINVAL;
+  }
+  int dev = -1;
+  cudaError_t ce = cudaGetDevice(&dev);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaGetDevice");
+  const int fbt = (F + 31) / 32;
+  const int fbw = blocks_fitting(c, prm, ws_bytes, fbt);
+  if (fbw < 1) { set_error("workspace too small for one 32-frame block"); return GFQ_EINVAL; }
+  if (prm->keep_messages && fbw < fbt) { set_error("keep_messages needs a workspace for all frames"); return GFQ_EINVAL; }
+  const Layout L = make_layout(c, fbw, prm);
+  const int q = c->q;
+
+  // Decoder constants: T and pi0 (doubles) into the workspace.
+  std::vector<double> hbuf((size_t)q * q + q, 0.0);
+  if (prm->markov_T) memcpy(hbuf.data(), prm->markov_T, sizeof(double) * q * q);
+  for (int a = 0; a < q; ++a) hbuf[(size_t)q * q + a] = prm->src_pi0 ? prm->src_pi0[a] : 1.0 / q;
+  ce = cudaMemcpyAsync(at<double>(ws, L.T), hbuf.data(), sizeof(double) * q * q, cudaMemcpyHostToDevice, st);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpyAsync(at<double>(ws, L.pi0), hbuf.data() + (size_t)q * q, sizeof(double) * q, cudaMemcpyHostToDevice, st);
+  // (pageable H2D copies are staged before cudaMemcpyAsync returns, so hbuf may die here)
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(at<unsigned long long>(ws, L.stats), 0, 4 * sizeof(unsigned long long), st);
+  if (ce != cudaSuccess) return cuda_fail(ce, "upload decoder constants");
+
+  LagRing &ring = lag_ring();
+  unsigned long long launches = 0;
+  int rc = GFQ_OK;
+#define RUN(x)                 \
+  do {                         \
+    rc = (x);                  \
+    ++launches;                \
+    if (rc != GFQ_OK) return rc; \
+  } while (0)
+
+  for (int fb0 = 0; fb0 < fbt; fb0 += fbw) {
+    WaveArgs a;
+    memset(&a, 0, sizeof(a));
+    a.c = c->d;
+    a.fb0 = fb0;
+    a.nfb = std::min(fbw, fbt - fb0);
+    a.n_frames = F;
+    a.qmsg = at<float>(ws, L.qmsg);
+    a.rmsg = at<float>(ws, L.rmsg);
+    a.pi = at<float>(ws, L.pi);
+    a.hard = at<unsigned char>(ws, L.hard);
+    a.z = at<unsigned char>(ws, L.z);
+    a.xhat = at<unsigned char>(ws, L.xhat);
+    a.qall = at<float>(ws, L.qall);
+    a.iters = at<int>(ws, L.iters);
+    a.conv = at<int>(ws, L.conv);
+    a.unsat = at<int>(ws, L.unsat);
+    a.newconv = at<int>(ws, L.newconv);
+    a.active = at<int>(ws, L.active);
+    a.list = at<int>(ws, L.list);
+    a.nactive = at<int>(ws, L.nactive);
+    a.stats = at<unsigned long long>(ws, L.stats);
+    a.T = prm->markov_T ? at<double>(ws, L.T) : nullptr;
+    a.pi0 = at<double>(ws, L.pi0);
+    a.markov = prm->markov_T != nullptr;
+    a.early_exit = prm->early_exit ? 1 : 0;
+    a.t = 1;
+    float *qs[2] = {at<float>(ws, L.qs0), at<float>(ws, L.qs1)};
+
+    RUN(launch_frontend(a, mode, ch_param, obs, hard_in, pi_in, st));
+    RUN(launch_syndrome(a, st));
+    RUN(launch_init_msgs(a, st));
+    RUN(launch_init_state(a, st));
+    if (prm->max_iters == 0) {
+      RUN(launch_clip_priors(a, st));
+    }
+    int t_done = 0;
+    for (int t = 1; t <= prm->max_iters; ++t) {
+      // Early exit: stop once a readback from two iterations ago saw no block left.
+      if (a.early_exit && t > 3 && ring.ok) {
+        const int k = (t - 3) % LagRing::K;
+        ce = cudaEventSynchronize(ring.ev[k]);
+        if (ce != cudaSuccess) return cuda_fail(ce, "cudaEventSynchronize");
+        if (ring.host[k] == 0) break;
+      }
+      a.t = t;
+      a.qs_old = qs[(t - 1) & 1];
+      a.qs_new = qs[t & 1];
+      if (prm->schedule == GFQ_PUS) {
+        RUN(launch_cn(a, st));
+        RUN(launch_vn(a, st));
+      } else {
+        for (int lv = 0; lv < c->n_levels; ++lv) {
+          const int lb = c->level_ptr_h[lv], n = c->level_ptr_h[lv + 1] - lb;
+          if (n > 0) RUN(launch_sus_level(a, lb, n, st));
+        }
+      }
+      RUN(launch_test(a, st));
+      RUN(launch_finalize(a, 0, st));
+      RUN(launch_capture(a, out, Lout, 0, st));
+      RUN(launch_compact(a, st));
+      if (a.early_exit && ring.ok) {
+        const int k = (t - 1) % LagRing::K;
+        ce = cudaMemcpyAsync(ring.host + k, a.nactive, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+        if (ce == cudaSuccess) ce = cudaEventRecord(ring.ev[k], st);
+        if (ce != cudaSuccess) return cuda_fail(ce, "lag readback");
+      }
+      t_done = t;
+    }
+    (void)t_done;
+    RUN(launch_finalize(a, 1, st));
+    RUN(launch_capture(a, out, Lout, 0, st));
+    const long long nvalid = std::min<long long>((long long)a.nfb * 32, (long long)F - (long long)fb0 * 32);
+    ce = cudaMemcpyAsync(iters_out + (size_t)fb0 * 32, a.iters, sizeof(int) * nvalid, cudaMemcpyDeviceToDevice, st);
+    if (ce != cudaSuccess) return cuda_fail(ce, "copy iters");
+  }
+  RUN(launch_set_u64(at<unsigned long long>(ws, L.stats) + 3, launches + 1, st));
+#undef RUN
+  return GFQ_OK;
+}
+
+}  // namespace gfq
+
+using namespace gfq;
+
+extern "C" size_t gfq_workspace_bytes(const gfq_code *c, int n_frames, const gfq_params *prm) {
+  if (!c || !prm || n_frames < 0) return 0;
+  const int fb = std::max(1, (n_frames + 31) / 32);
+  return make_layout(c, fb, prm).total;
+}
+
+static size_t obs_bytes(const gfq_code *c, int F, const gfq_params *prm) {
+  const size_t Mp = (size_t)c->M * c->p;
+  return (size_t)F * Mp * (prm->channel == GFQ_BIAWGN ? sizeof(float) : 1);
+}
+
+extern "C" size_t gfq_workspace_bytes_host(const gfq_code *c, int n_frames, const gfq_params *prm) {
+  if (!c || !prm || n_frames < 0) return 0;
+  return al256(obs_bytes(c, n_frames, prm)) + al256((size_t)n_frames * c->N) +
+         al256((size_t)n_frames * sizeof(int)) + gfq_workspace_bytes(c, n_frames, prm);
+}
+
+extern "C" int gfq_decode(const gfq_code *c, int n_frames, const void *obs, const gfq_params *prm,
+                          unsigned char *s_hat, int *iters, void *ws, size_t ws_bytes, void *stream) {
+  int rc = check_params(c, prm, true);
+  if (rc) return rc;
+  return decode_common(c, n_frames, prm->channel, prm->ch_param, obs, nullptr, nullptr, prm, s_hat,
+                       c->N, iters, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int gfq_decode_evidence(const gfq_code *c, int n_frames, const unsigned char *hard_bits,
+                                   const float *bit_flip_prob, const gfq_params *prm,
+                                   unsigned char *x_hat, int *iters, void *ws, size_t ws_bytes,
+                                   void *stream) {
+  int rc = check_params(c, prm, false);
+  if (rc) return rc;
+  return decode_common(c, n_frames, 3, 0.0, nullptr, hard_bits, bit_flip_prob, prm, x_hat, c->V, iters,
+                       ws, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int gfq_decode_host(const gfq_code *c, int n_frames, const void *obs_host,
+                               const gfq_params *prm, unsigned char *s_hat_host, int *iters_host,
+                               void *ws, size_t ws_bytes, void *stream) {
+  int rc = check_params(c, prm, true);
+  if (rc) return rc;
+  if (n_frames < 0) { set_error("n_frames < 0"); return GFQ_EINVAL; }
+  if (n_frames == 0) return GFQ_OK;
+  if (!obs_host || !s_hat_host || !iters_host || !ws) { set_error("NULL buffer"); return GFQ_EINVAL; }
+  const size_t ob = al256(obs_bytes(c, n_frames, prm));
+  const size_t sb = al256((size_t)n_frames * c->N);
+  const size_t ib = al256((size_t)n_frames * sizeof(int));
+  if (ws_bytes < ob + sb + ib + gfq_workspace_bytes(c, 1, prm)) {
+    set_error("workspace too small (size it with gfq_workspace_bytes_host)");
+    return GFQ_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  char *base = (char *)ws;
+  void *obs_d = base;
+  unsigned char *s_d = (unsigned char *)(base + ob);
+  int *it_d = (int *)(base + ob + sb);
+  cudaError_t ce = cudaMemcpyAsync(obs_d, obs_host, obs_bytes(c, n_frames, prm), cudaMemcpyHostToDevice, st);
+  if (ce != cudaSuccess) return cuda_fail(ce, "copy obs to device");
+  rc = decode_common(c, n_frames, prm->channel, prm->ch_param, obs_d, nullptr, nullptr, prm, s_d, c->N,
+                     it_d, base + ob + sb + ib, ws_bytes - (ob + sb + ib), st);
+  if (rc) return rc;
+  ce = cudaMemcpyAsync(s_hat_host, s_d, (size_t)n_frames * c->N, cudaMemcpyDeviceToHost, st);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(iters_host, it_d, sizeof(int) * n_frames, cudaMemcpyDeviceToHost, st);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+  if (ce != cudaSuccess) return cuda_fail(ce, "copy results to host");
+  return GFQ_OK;
+}
+
+extern "C" int gfq_export_messages(const gfq_code *c, int n_frames, const void *ws, size_t ws_bytes,
+                                   const gfq_params *prm, float *q_msg, float *r_msg, float *Q,
+                                   void *stream) {
+  int rc = check_params(c, prm, false);
+  if (rc) return rc;
+  if (!ws || n_frames < 0) { set_error("bad workspace or n_frames"); return GFQ_EINVAL; }
+  if (!prm->keep_messages) { set_error("export needs params.keep_messages = 1"); return GFQ_EINVAL; }
+  const int fbt = (n_frames + 31) / 32;
+  if (n_frames == 0) return GFQ_OK;
+  const Layout L = make_layout(c, fbt, prm);
+  if (L.total > ws_bytes) { set_error("workspace does not hold all frames"); return GFQ_EINVAL; }
+  WaveArgs a;
+  memset(&a, 0, sizeof(a));
+  a.c = c->d;
+  a.fb0 = 0;
+  a.nfb = fbt;
+  a.n_frames = n_frames;
+  void *w = const_cast<void *>(ws);
+  a.qmsg = at<float>(w, L.qmsg);
+  a.rmsg = at<float>(w, L.rmsg);
+  a.qall = at<float>(w, L.qall);
+  return launch_export(a, q_msg, r_msg, Q, (cudaStream_t)stream);
+}
+
+extern "C" int gfq_decode_stats(const gfq_code *c, const void *ws, size_t ws_bytes, long long stats[4],
+                                void *stream) {
+  if (!c || !ws || !stats) { set_error("NULL argument"); return GFQ_EINVAL; }
+  if (ws_bytes < 4 * sizeof(unsigned long long)) { set_error("workspace too small"); return GFQ_EINVAL; }
+  unsigned long long h[4];
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t ce = cudaMemcpyAsync(h, ws, sizeof(h), cudaMemcpyDeviceToHost, st);  // stats live at offset 0
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+  if (ce != cudaSuccess) return cuda_fail(ce, "gfq_decode_stats");
+  for (int k = 0; k < 4; ++k) stats[k] = (long long)h[k];
+  return GFQ_OK;
+}

@@ -1,0 +1,113 @@
+// gfq_internal.cuh -- shared declarations of the libgfq CUDA implementation.
+//
+// Data layout in HBM: frames are processed in
+// blocks of 32 (one frame per lane: every warp of a task works on the same
+// check / variable for 32 different frames, so all control flow and all
+// graph indices are warp-uniform).  Every per-frame quantity is stored as
+// [frame block][item][entry][32 lanes], so one (item, entry) row of a block
+// is a contiguous 128-byte line (floats) and any per-edge permutation of a
+// q-vector's entries is just a choice of which rows to load or store.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/gfq.h"
+
+namespace gfq {
+
+constexpr int kLanes = 32;  // frames per block
+constexpr int kMaxDeg = 8;  // supported check / variable degree
+
+// -------------------------------------------------------------- code object
+struct DevCode {
+  int p, q, N, M, V;
+  long long E;
+  int max_cdeg, max_vdeg;
+  const int *row_ptr;        // [M+1]   edges of check i: row_ptr[i]..row_ptr[i+1]-1
+  const int *edge_var;       // [E]     variable j of edge e (check-major edge ids)
+  const int *edge_check;     // [E]     check i of edge e
+  const unsigned long long *edge_perm;  // [E] packed bytes h_e^-1 * 2^b, b < p
+  const unsigned char *edge_coef;       // [E] h_e
+  const int *col_ptr;        // [V+1]
+  const int *col_edge;       // [E]     edges of variable j (ascending check) == canonical order
+  const int *level_ptr;      // [L+1]   SUS dependency levels
+  const int *level_cols;     // [V]
+  const unsigned char *mul;  // [q*q]   GF(2^p) product table
+};
+
+}  // namespace gfq
+
+struct gfq_code {
+  int p, q, N, M, V;
+  unsigned poly;
+  long long E;
+  int max_cdeg, max_vdeg, n_levels;
+  int device;
+  std::vector<int> level_ptr_h;
+  void *dev_blob;  // one cudaMalloc holding every device table
+  gfq::DevCode d;
+};
+
+namespace gfq {
+
+void set_error(const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+
+// -------------------------------------------------------------- workspace
+struct Layout {
+  int fbw;            // frame blocks per wave
+  size_t qmsg, rmsg, pi, hard, z, xhat, qs0, qs1, qall, iters, conv, unsat, newconv;
+  size_t active, list, nactive, stats, T, pi0, total;
+};
+Layout make_layout(const gfq_code *c, int fbw, const gfq_params *prm);
+
+// -------------------------------------------------------------- kernel args
+struct WaveArgs {
+  DevCode c;
+  int fb0;          // first frame block of this wave (global)
+  int nfb;          // blocks in this wave
+  int n_frames;     // total frames of the call
+  float *qmsg;      // [nfb][E][q][32]
+  float *rmsg;      // [nfb][E][q][32] or null (SUS without keep)
+  float *pi;        // [nfb][M*p][32] per-bit flip probability
+  unsigned char *hard;  // [nfb][M*p][32]
+  unsigned char *z;     // [nfb][M][32]
+  unsigned char *xhat;  // [nfb][V][32]
+  float *qs_old, *qs_new;  // [nfb][N][q][32] Markov posterior snapshots (or null)
+  float *qall;          // [nfb][V][q][32] or null
+  int *iters;           // [nfb*32] first passing t, -1
+  int *conv;            // [nfb*32] 1 once converged (or invalid lane)
+  int *unsat;           // [nfb*32]
+  int *newconv;         // [nfb*32]
+  int *active;          // [nfb]
+  int *list;            // [nfb] active block ids (wave-local)
+  int *nactive;         // [1]
+  unsigned long long *stats;  // [4]
+  const double *T;      // [q*q] or null
+  const double *pi0;    // [q]
+  int markov;
+  int t;                // current iteration (1-based)
+  int early_exit;
+};
+
+// launchers (gfq_kernels.cu)
+int launch_frontend(const WaveArgs &a, int mode, double ch_param, const void *obs,
+                    const unsigned char *hard_in, const float *pi_in, cudaStream_t s);
+int launch_syndrome(const WaveArgs &a, cudaStream_t s);
+int launch_init_msgs(const WaveArgs &a, cudaStream_t s);
+int launch_init_state(const WaveArgs &a, cudaStream_t s);
+int launch_cn(const WaveArgs &a, cudaStream_t s);
+int launch_vn(const WaveArgs &a, cudaStream_t s);
+int launch_sus_level(const WaveArgs &a, int level, int ncols, cudaStream_t s);
+int launch_test(const WaveArgs &a, cudaStream_t s);
+int launch_finalize(const WaveArgs &a, int final_pass, cudaStream_t s);
+int launch_capture(const WaveArgs &a, unsigned char *out, int L, int mode, cudaStream_t s);
+int launch_compact(const WaveArgs &a, cudaStream_t s);
+int launch_clip_priors(const WaveArgs &a, cudaStream_t s);
+int launch_export(const WaveArgs &a, float *q_out, float *r_out, float *Q_out, cudaStream_t s);
+int launch_set_u64(unsigned long long *p, unsigned long long v, cudaStream_t s);
+
+}  // namespace gfq

@@ -1,0 +1,208 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the
+same seeded inputs.  Gates (BASELINE.json north_star):
+  * message gate: after a fixed 5 iterations every q, r, Q message within
+    max-abs 1e-4, PUS and SUS, every config (C5 on a subset);
+  * decision gate: hard decisions and iterations-to-convergence identical on
+    >= 99.9 % of frames (reading A18: frames that fail in both are matched on
+    the iteration count only).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+MSG_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def gfq():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_cs_0605069_b200 import gfq as g
+    return g
+
+
+def _setup(name, nframes, point=0, first=0):
+    cfg = synth.CONFIGS[name]
+    code = synth.code_for(cfg)
+    fr = synth.frames_for(cfg, code, range(first, first + nframes), point=point)
+    return cfg, code, fr
+
+
+def _channel(gfq, fr):
+    return {synth.BSC: gfq.GFQ_BSC, synth.BEC: gfq.GFQ_BEC, synth.BIAWGN: gfq.GFQ_BIAWGN}[fr.channel]
+
+
+def _gpu_decode(gfq, gcode, fr, schedule, max_iters, early_exit, T=None, keep=False):
+    prm = gfq.Params(_channel(gfq, fr), fr.ch_param, schedule, max_iters, early_exit=early_exit,
+                     markov_T=T, keep_messages=keep)
+    obs = torch.as_tensor(fr.obs).cuda()
+    s_hat, iters, ws = gfq.gfq_decode(gcode, obs, prm)
+    torch.cuda.synchronize()
+    return prm, s_hat.cpu().numpy(), iters.cpu().numpy(), ws
+
+
+MSG_CASES = [("C1", 64, 0), ("C2", 80, 0), ("C3", 40, 0), ("C3", 40, 5), ("C4", 40, 0), ("C5", 8, 0)]
+
+
+@pytest.mark.parametrize("schedule", [0, 1], ids=["PUS", "SUS"])
+@pytest.mark.parametrize("name,nframes,point", MSG_CASES)
+def test_message_gate_5_iterations(gfq, name, nframes, point, schedule):
+    cfg, code, fr = _setup(name, nframes, point)
+    T = synth.markov_T_for(cfg)
+    gcode = gfq.Code.from_synth(code)
+    prm, s_hat, iters, ws = _gpu_decode(gfq, gcode, fr, schedule, 5, False, T, keep=True)
+    qg, rg, Qg = gfq.gfq_export_messages(gcode, fr.F, ws, prm)
+    qg, rg, Qg = qg.cpu().numpy(), rg.cpu().numpy(), Qg.cpu().numpy()
+    oc = oracle.OCode.from_synth(code)
+    hard, pi = oracle.frontend(fr.channel, fr.ch_param, fr.obs)
+    ref = oc.decode(hard, pi, schedule=schedule, max_iters=5, fixed=True, T=T, keep_messages=True)
+    errs = {k: float(np.max(np.abs(g - ref[k]))) for k, g in (("q", qg), ("r", rg), ("Q", Qg))}
+    print(name, point, "PUS" if schedule == 0 else "SUS", errs,
+          "p99 q err %.3g" % np.percentile(np.abs(qg - ref["q"]), 99))
+    assert max(errs.values()) <= MSG_TOL, errs
+    assert np.array_equal(iters, ref["iters"])
+    st = gfq.gfq_decode_stats(gcode, ws)
+    assert st["zero_normalisers"] == 0
+
+
+def _decision_match(gpu_x, gpu_it, ref_x, ref_it):
+    """Reading A18: a frame matches if both converge at the same t with identical x, or neither converges."""
+    both_fail = (gpu_it == -1) & (ref_it == -1)
+    same = (gpu_it == ref_it) & np.all(gpu_x == ref_x, axis=1)
+    return both_fail | same, same
+
+
+DEC_CASES = [("C1", 64, 0), ("C2", 256, 0), ("C3", 128, 1), ("C3", 128, 4), ("C4", 64, 0), ("C5", 8, 0)]
+
+
+@pytest.mark.parametrize("schedule", [0, 1], ids=["PUS", "SUS"])
+@pytest.mark.parametrize("name,nframes,point", DEC_CASES)
+def test_decision_gate(gfq, name, nframes, point, schedule):
+    cfg, code, fr = _setup(name, nframes, point)
+    T = synth.markov_T_for(cfg)
+    gcode = gfq.Code.from_synth(code)
+    _, s_hat, iters, ws = _gpu_decode(gfq, gcode, fr, schedule, cfg.max_iters, True, T)
+    oc = oracle.OCode.from_synth(code)
+    hard, pi = oracle.frontend(fr.channel, fr.ch_param, fr.obs)
+    ref = oc.decode(hard, pi, schedule=schedule, max_iters=cfg.max_iters, T=T)
+    match, strict = _decision_match(s_hat, iters, ref["xhat"][:, :code.N], ref["iters"])
+    allowed = int(np.floor(0.001 * fr.F))
+    print(name, point, "mismatch", int((~match).sum()), "strict", int((~strict).sum()),
+          "mean iters gpu %.2f ref %.2f" % (iters[iters > 0].mean() if (iters > 0).any() else -1,
+                                            ref["iters"][ref["iters"] > 0].mean() if (ref["iters"] > 0).any() else -1))
+    assert int((~match).sum()) <= allowed
+    assert gfq.gfq_decode_stats(gcode, ws)["zero_normalisers"] == 0
+
+
+def test_evidence_entry_matches_oracle(gfq):
+    """gfq_decode_evidence with the oracle's own front end (pi rounded to fp32, widened
+    back exactly on the oracle side): bit-identical evidence on both sides."""
+    cfg, code, fr = _setup("C3", 40, 2)
+    gcode = gfq.Code.from_synth(code)
+    hard, pi = oracle.frontend(fr.channel, fr.ch_param, fr.obs)
+    pi32 = pi.astype(np.float32)
+    for schedule in (0, 1):
+        prm = gfq.Params(schedule=schedule, max_iters=5, early_exit=False, keep_messages=True)
+        x, it, ws = gfq.gfq_decode_evidence(gcode, torch.as_tensor(hard).cuda(), torch.as_tensor(pi32).cuda(), prm)
+        qg, rg, Qg = gfq.gfq_export_messages(gcode, fr.F, ws, prm)
+        ref = oracle.OCode.from_synth(code).decode(hard, pi32.astype(np.float64), schedule=schedule,
+                                                   max_iters=5, fixed=True, keep_messages=True)
+        assert float(np.max(np.abs(qg.cpu().numpy() - ref["q"]))) <= MSG_TOL
+        assert float(np.max(np.abs(Qg.cpu().numpy() - ref["Q"]))) <= MSG_TOL
+        assert np.array_equal(it.cpu().numpy(), ref["iters"])
+
+
+@pytest.mark.parametrize("name,full", [("C2", 1024), ("C4", 8192)])
+def test_full_size_sampled(gfq, name, full):
+    """BASELINE.json full batch on the GPU (the bench's launch configuration); the
+    oracle recomputes a sample of frames one by one (frames are independent)."""
+    cfg = synth.CONFIGS[name]
+    code = synth.code_for(cfg)
+    fr = synth.frames_for(cfg, code, range(full))
+    T = synth.markov_T_for(cfg)
+    gcode = gfq.Code.from_synth(code)
+    sample = np.linspace(0, full - 1, 12).astype(int)
+    oc = oracle.OCode.from_synth(code)
+    hard, pi = oracle.frontend(fr.channel, fr.ch_param, fr.obs[sample])
+    for schedule in (0, 1):
+        _, s_hat, iters, _ = _gpu_decode(gfq, gcode, fr, schedule, cfg.max_iters, True, T)
+        ref = oc.decode(hard, pi, schedule=schedule, max_iters=cfg.max_iters, T=T)
+        match, _ = _decision_match(s_hat[sample], iters[sample], ref["xhat"][:, :code.N], ref["iters"])
+        assert match.all()
+
+
+def test_edge_cases(gfq):
+    cfg, code, fr = _setup("C1", 33)           # ragged: 2 blocks, 1 valid lane in the last
+    gcode = gfq.Code.from_synth(code)
+    oc = oracle.OCode.from_synth(code)
+    hard, pi = oracle.frontend(fr.channel, fr.ch_param, fr.obs)
+    # max_iters = 0: iters -1 and clipped priors
+    _, s0, it0, _ = _gpu_decode(gfq, gcode, fr, 0, 0, True)
+    ref0 = oc.decode(hard, pi, max_iters=0)
+    assert (it0 == -1).all() and np.array_equal(s0, ref0["xhat"][:, :code.N])
+    # single frame
+    fr1 = synth.frames_for(cfg, code, [7])
+    _, s1, it1, _ = _gpu_decode(gfq, gcode, fr1, 1, 100, True)
+    h1, p1 = oracle.frontend(fr1.channel, fr1.ch_param, fr1.obs)
+    r1 = oc.decode(h1, p1, schedule=1, max_iters=100)
+    assert it1[0] == r1["iters"][0] and np.array_equal(s1[0], r1["xhat"][0, :code.N])
+    # zero frames is a no-op
+    prm = gfq.Params(gfq.GFQ_BSC, fr.ch_param, 0, 10)
+    empty = torch.empty((0, code.M), dtype=torch.uint8, device="cuda")
+    s, it, _ = gfq.gfq_decode(gcode, empty, prm, workspace=gfq.alloc_workspace(1 << 20))
+    assert s.shape[0] == 0
+    # fixed mode reports the same first-passing t and estimate as early exit
+    for sched in (0, 1):
+        _, sa, ia, _ = _gpu_decode(gfq, gcode, fr, sched, 60, True)
+        _, sb, ib, _ = _gpu_decode(gfq, gcode, fr, sched, 60, False)
+        assert np.array_equal(ia, ib) and np.array_equal(sa, sb)
+
+
+def test_waves_and_determinism(gfq):
+    """A workspace for 1 block (3 waves) gives the same bits as one wave; reruns are identical."""
+    cfg, code, fr = _setup("C2", 70)
+    T = synth.markov_T_for(cfg)
+    gcode = gfq.Code.from_synth(code)
+    obs = torch.as_tensor(fr.obs).cuda()
+    for sched in (0, 1):
+        prm = gfq.Params(gfq.GFQ_BSC, fr.ch_param, sched, cfg.max_iters, markov_T=T)
+        a = gfq.gfq_decode(gcode, obs, prm)
+        b = gfq.gfq_decode(gcode, obs, prm)
+        small = gfq.alloc_workspace(gfq.gfq_workspace_bytes(gcode, 32, prm))
+        c = gfq.gfq_decode(gcode, obs, prm, workspace=small)
+        torch.cuda.synchronize()
+        for x, y in ((a, b), (a, c)):
+            assert torch.equal(x[0], y[0]) and torch.equal(x[1], y[1])
+
+
+def test_host_entry_matches_device(gfq):
+    cfg, code, fr = _setup("C3", 64, 3)
+    gcode = gfq.Code.from_synth(code)
+    prm = gfq.Params(gfq.GFQ_BIAWGN, fr.ch_param, 0, cfg.max_iters)
+    sd, itd, _ = gfq.gfq_decode(gcode, torch.as_tensor(fr.obs).cuda(), prm)
+    sh, ith, _ = gfq.gfq_decode_host(gcode, torch.as_tensor(fr.obs).pin_memory(), prm)
+    assert torch.equal(sd.cpu(), sh) and torch.equal(itd.cpu(), ith)
+
+
+def test_natural_chain_labelling_many_levels(gfq):
+    """B chain in natural order: the SUS dependency depth is ~M (serial); still exact."""
+    cfg = synth.CONFIGS["C2"]
+    code = synth.make_code(cfg.p, 300, 600, 77, permute_noise=False)
+    fr = synth.make_frames(code, 9, range(40), "markov", synth.BSC, 0.05, stay=0.85)
+    T = synth.markov_uniform_jump(code.q, 0.85)
+    gcode = gfq.Code.from_synth(code)
+    assert gcode.sus_levels > 500
+    prm, s_hat, iters, ws = _gpu_decode(gfq, gcode, fr, 1, 5, False, T, keep=True)
+    qg, rg, Qg = gfq.gfq_export_messages(gcode, fr.F, ws, prm)
+    oc = oracle.OCode.from_synth(code)
+    hard, pi = oracle.frontend(fr.channel, fr.ch_param, fr.obs)
+    ref = oc.decode(hard, pi, schedule=1, max_iters=5, fixed=True, T=T, keep_messages=True)
+    assert float(np.max(np.abs(qg.cpu().numpy() - ref["q"]))) <= MSG_TOL
+    assert float(np.max(np.abs(Qg.cpu().numpy() - ref["Q"]))) <= MSG_TOL
