@@ -178,6 +178,19 @@ int gfq_export_messages(const gfq_code *code, int n_frames, const void *workspac
 int gfq_decode_stats(const gfq_code *code, const void *workspace, size_t ws_bytes,
                      long long stats[4], void *stream);
 
+/* Per-kernel timing for roofline reporting.  gfq_profile_enable(1) makes every
+ * later decode call of the calling thread record a CUDA event pair around each
+ * kernel it launches, on the decode's stream (accumulators are reset);
+ * gfq_profile_enable(0) stops recording.  gfq_profile_read synchronises the
+ * recorded events and writes, per kernel kind k < GFQ_NKERNELS, the summed
+ * duration in ms (ms[k]) and the number of launches (launches[k]); NULL outputs
+ * are skipped.  gfq_kernel_name(k) names kind k ("cn", "vn", "sus", ...) or
+ * returns NULL for k out of range. */
+#define GFQ_NKERNELS 13
+int gfq_profile_enable(int on);
+int gfq_profile_read(double *ms, long long *launches);
+const char *gfq_kernel_name(int kind);
+
 #ifdef __cplusplus
 }
 #endif

@@ -151,8 +151,12 @@ int o_var_node(int q, int dv, const double *prior, const double *rin, int out,
     return 0;
 }
 
+/* Tie tolerance of the clipping step (reading A17 in DESIGN.md). */
+#define O_TIE_REL 1e-5
+
 /* Pseudo-posterior, Eq. (5): Q_j^a = alpha_j p_j^a prod_i r_ij^a,
- * then "clipping": x_j = the a maximising Q_j (ties -> smallest a, A17).
+ * then "clipping": x_j = the a maximising Q_j (ties -> smallest a, where
+ * values within a relative O_TIE_REL of the maximum count as ties, A17).
  * Returns x_j; *zero_norm set to 1 if the normaliser vanished (A19). */
 int o_posterior(int q, int dv, const double *prior, const double *rin,
                 double *Q, int *zero_norm)
@@ -171,9 +175,13 @@ int o_posterior(int q, int dv, const double *prior, const double *rin,
     } else {
         for (int a = 0; a < q; ++a) Q[a] /= s;
     }
+    /* ties -> smallest a; values equal up to round-off (relative O_TIE_REL) are ties */
+    double mx = 0.0;
+    for (int a = 0; a < q; ++a)
+        if (Q[a] > mx) mx = Q[a];
     int best = 0;
-    for (int a = 1; a < q; ++a)
-        if (Q[a] > Q[best]) best = a;
+    for (int a = 0; a < q; ++a)
+        if (Q[a] >= mx * (1.0 - O_TIE_REL)) { best = a; break; }
     return best;
 }
 
@@ -391,9 +399,13 @@ int o_decode_frame(const ocode *c, int schedule, int max_iters, int fixed,
     *iters = -1;
     if (max_iters <= 0) { /* clip the priors */
         for (int j = 0; j < V; ++j) {
+            const double *pj = prior + (size_t)j * q;
+            double mx = 0.0;
+            for (int a = 0; a < q; ++a)
+                if (pj[a] > mx) mx = pj[a];
             int best = 0;
-            for (int a = 1; a < q; ++a)
-                if (prior[(size_t)j * q + a] > prior[(size_t)j * q + best]) best = a;
+            for (int a = 0; a < q; ++a)
+                if (pj[a] >= mx * (1.0 - O_TIE_REL)) { best = a; break; }
             xhat[j] = (uint8_t)best;
             memcpy(Q + (size_t)j * q, prior + (size_t)j * q, sizeof(double) * (size_t)q);
         }

@@ -113,6 +113,47 @@ static T *at(void *ws, size_t off) {
   return off == kNone ? nullptr : (T *)((char *)ws + off);
 }
 
+// ---------------------------------------------------------------- profiling
+enum Kind { K_FRONTEND, K_SYNDROME, K_INIT_MSGS, K_INIT_STATE, K_CN, K_VN, K_SUS, K_TEST, K_FINALIZE,
+            K_CAPTURE, K_COMPACT, K_CLIP, K_OTHER, K_N };
+static const char *kKindNames[K_N] = {"frontend", "syndrome", "init_msgs", "init_state", "cn", "vn",
+                                      "sus", "test", "finalize", "capture", "compact", "clip", "other"};
+static_assert(K_N == GFQ_NKERNELS, "kernel kinds");
+
+struct Profiler {
+  bool on = false;
+  struct Rec { int kind; cudaEvent_t a, b; };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  double ms[K_N] = {0};
+  long long n[K_N] = {0};
+  cudaEvent_t get() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    return e;
+  }
+  int drain() {
+    for (auto &r : pending) {
+      float t = 0.f;
+      cudaError_t ce = cudaEventSynchronize(r.b);
+      if (ce == cudaSuccess) ce = cudaEventElapsedTime(&t, r.a, r.b);
+      if (ce != cudaSuccess) return cuda_fail(ce, "gfq_profile_read");
+      ms[r.kind] += t;
+      n[r.kind] += 1;
+      pool.push_back(r.a);
+      pool.push_back(r.b);
+    }
+    pending.clear();
+    return GFQ_OK;
+  }
+};
+
+static Profiler &profiler() {
+  static thread_local Profiler p;
+  return p;
+}
+
 struct LagRing {
   static constexpr int K = 8;
   cudaEvent_t ev[K];
@@ -166,11 +207,20 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
   LagRing &ring = lag_ring();
   unsigned long long launches = 0;
   int rc = GFQ_OK;
-#define RUN(x)                 \
-  do {                         \
-    rc = (x);                  \
-    ++launches;                \
-    if (rc != GFQ_OK) return rc; \
+  Profiler &prof = profiler();
+#define RUN(kind, x)                                                         \
+  do {                                                                       \
+    cudaEvent_t e0_ = nullptr, e1_ = nullptr;                                \
+    if (prof.on) { e0_ = prof.get(); e1_ = prof.get(); }                     \
+    if (e0_ && e1_) cudaEventRecord(e0_, st);                                \
+    rc = (x);                                                                \
+    ++launches;                                                              \
+    if (e0_ && e1_) {                                                        \
+      cudaEventRecord(e1_, st);                                              \
+      prof.pending.push_back({(kind), e0_, e1_});                            \
+      if (prof.pending.size() > 4096 && prof.drain() != GFQ_OK) return GFQ_ECUDA; \
+    }                                                                        \
+    if (rc != GFQ_OK) return rc;                                             \
   } while (0)
 
   for (int fb0 = 0; fb0 < fbt; fb0 += fbw) {
@@ -202,12 +252,15 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
     a.t = 1;
     float *qs[2] = {at<float>(ws, L.qs0), at<float>(ws, L.qs1)};
 
-    RUN(launch_frontend(a, mode, ch_param, obs, hard_in, pi_in, st));
-    RUN(launch_syndrome(a, st));
-    RUN(launch_init_msgs(a, st));
-    RUN(launch_init_state(a, st));
+    // estimates of lanes that never run (invalid lanes of a ragged block) read as 0
+    ce = cudaMemsetAsync(a.xhat, 0, (size_t)a.nfb * c->V * 32, st);
+    if (ce != cudaSuccess) return cuda_fail(ce, "clear x_hat");
+    RUN(K_FRONTEND, launch_frontend(a, mode, ch_param, obs, hard_in, pi_in, st));
+    RUN(K_SYNDROME, launch_syndrome(a, st));
+    RUN(K_INIT_MSGS, launch_init_msgs(a, st));
+    RUN(K_INIT_STATE, launch_init_state(a, st));
     if (prm->max_iters == 0) {
-      RUN(launch_clip_priors(a, st));
+      RUN(K_CLIP, launch_clip_priors(a, st));
     }
     int t_done = 0;
     for (int t = 1; t <= prm->max_iters; ++t) {
@@ -222,18 +275,18 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
       a.qs_old = qs[(t - 1) & 1];
       a.qs_new = qs[t & 1];
       if (prm->schedule == GFQ_PUS) {
-        RUN(launch_cn(a, st));
-        RUN(launch_vn(a, st));
+        RUN(K_CN, launch_cn(a, st));
+        RUN(K_VN, launch_vn(a, st));
       } else {
         for (int lv = 0; lv < c->n_levels; ++lv) {
           const int lb = c->level_ptr_h[lv], n = c->level_ptr_h[lv + 1] - lb;
-          if (n > 0) RUN(launch_sus_level(a, lb, n, st));
+          if (n > 0) RUN(K_SUS, launch_sus_level(a, lb, n, st));
         }
       }
-      RUN(launch_test(a, st));
-      RUN(launch_finalize(a, 0, st));
-      RUN(launch_capture(a, out, Lout, 0, st));
-      RUN(launch_compact(a, st));
+      RUN(K_TEST, launch_test(a, st));
+      RUN(K_FINALIZE, launch_finalize(a, 0, st));
+      RUN(K_CAPTURE, launch_capture(a, out, Lout, 0, st));
+      RUN(K_COMPACT, launch_compact(a, st));
       if (a.early_exit && ring.ok) {
         const int k = (t - 1) % LagRing::K;
         ce = cudaMemcpyAsync(ring.host + k, a.nactive, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
@@ -243,13 +296,13 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
       t_done = t;
     }
     (void)t_done;
-    RUN(launch_finalize(a, 1, st));
-    RUN(launch_capture(a, out, Lout, 0, st));
+    RUN(K_FINALIZE, launch_finalize(a, 1, st));
+    RUN(K_CAPTURE, launch_capture(a, out, Lout, 0, st));
     const long long nvalid = std::min<long long>((long long)a.nfb * 32, (long long)F - (long long)fb0 * 32);
     ce = cudaMemcpyAsync(iters_out + (size_t)fb0 * 32, a.iters, sizeof(int) * nvalid, cudaMemcpyDeviceToDevice, st);
     if (ce != cudaSuccess) return cuda_fail(ce, "copy iters");
   }
-  RUN(launch_set_u64(at<unsigned long long>(ws, L.stats) + 3, launches + 1, st));
+  RUN(K_OTHER, launch_set_u64(at<unsigned long long>(ws, L.stats) + 3, launches + 1, st));
 #undef RUN
   return GFQ_OK;
 }
@@ -360,4 +413,30 @@ extern "C" int gfq_decode_stats(const gfq_code *c, const void *ws, size_t ws_byt
   if (ce != cudaSuccess) return cuda_fail(ce, "gfq_decode_stats");
   for (int k = 0; k < 4; ++k) stats[k] = (long long)h[k];
   return GFQ_OK;
+}
+
+extern "C" int gfq_profile_enable(int on) {
+  Profiler &p = profiler();
+  if (on) {
+    int rc = p.drain();
+    if (rc) return rc;
+    for (int k = 0; k < K_N; ++k) { p.ms[k] = 0.0; p.n[k] = 0; }
+  }
+  p.on = on != 0;
+  return GFQ_OK;
+}
+
+extern "C" int gfq_profile_read(double *ms, long long *launches) {
+  Profiler &p = profiler();
+  int rc = p.drain();
+  if (rc) return rc;
+  for (int k = 0; k < K_N; ++k) {
+    if (ms) ms[k] = p.ms[k];
+    if (launches) launches[k] = p.n[k];
+  }
+  return GFQ_OK;
+}
+
+extern "C" const char *gfq_kernel_name(int kind) {
+  return (kind >= 0 && kind < K_N) ? kKindNames[kind] : nullptr;
 }

@@ -28,6 +28,10 @@
 
 namespace gfq {
 
+// Relative tolerance under which two posterior values count as a tie in the
+// clipping step (reading A17; the oracle applies the same rule).
+constexpr double kTieRel = 1e-5;
+
 // ============================================================== configuration
 template <int Q>
 struct QC {
@@ -87,6 +91,13 @@ __device__ __forceinline__ int row_lo(const int (&bb)[P], int k) {  // contribut
   for (int b = 0; b < LKR; ++b)
     if ((k >> b) & 1) r ^= bb[b];
   return r;
+}
+
+// Early exit freezes a converged frame: its lane keeps computing (warp-uniform
+// control flow) but stores nothing.  Invalid lanes of a ragged last block are
+// marked converged from the start.
+__device__ __forceinline__ bool lane_frozen(const WaveArgs &a, int fb, int lane) {
+  return a.early_exit && a.conv[fb * 32 + lane] != 0;
 }
 
 __device__ __forceinline__ double neg_if(double v, int s) {
@@ -213,7 +224,7 @@ __device__ __forceinline__ void load_prior(const WaveArgs &a, int fb, int j, int
 template <int Q, int DVMAX, bool MARKOV>
 __device__ __forceinline__ void vn_body(const WaveArgs &a, int fb, int j, int e0, int dv,
                                         double (&r)[DVMAX][QC<Q>::KR], double *red, int g,
-                                        int c, int lane) {
+                                        int c, int lane, bool frozen) {
   using C = QC<Q>;
   constexpr int KR = C::KR, T = C::T;
   const long long E = a.c.E;
@@ -233,8 +244,7 @@ __device__ __forceinline__ void vn_body(const WaveArgs &a, int fb, int j, int e0
   double sums[DVMAX + 1];
 #pragma unroll
   for (int s = 0; s <= DVMAX; ++s) sums[s] = 0.0;
-  double best = -1.0;
-  int bidx = 0;
+  double best = 0.0;
 #pragma unroll
   for (int k = 0; k < KR; ++k) {
 #pragma unroll
@@ -244,15 +254,14 @@ __device__ __forceinline__ void vn_body(const WaveArgs &a, int fb, int j, int e0
         sums[s] += r[s][k];
       }
     sums[DVMAX] += tot[k];
-    if (tot[k] > best) { best = tot[k]; bidx = c * KR + k; }
+    best = fmax(best, tot[k]);
   }
   if constexpr (T > 1) {
-    // cross-warp reduction of the sums and of the argmax
+    // cross-warp reduction of the sums and of the maximum
 #pragma unroll
     for (int s = 0; s <= DVMAX; ++s)
       if (s < dv || s == DVMAX) red[((size_t)s * T + c) * 32 + lane] = sums[s];
     red[((size_t)(DVMAX + 1) * T + c) * 32 + lane] = best;
-    ((int *)(red + (size_t)(DVMAX + 2) * T * 32))[c * 32 + lane] = bidx;
     group_bar<T>(g);
 #pragma unroll
     for (int s = 0; s <= DVMAX; ++s)
@@ -262,13 +271,25 @@ __device__ __forceinline__ void vn_body(const WaveArgs &a, int fb, int j, int e0
         for (int cc = 0; cc < T; ++cc) t += red[((size_t)s * T + cc) * 32 + lane];
         sums[s] = t;
       }
-    best = -1.0;
 #pragma unroll
-    for (int cc = 0; cc < T; ++cc) {
-      const double v = red[((size_t)(DVMAX + 1) * T + cc) * 32 + lane];
-      if (v > best) { best = v; bidx = ((int *)(red + (size_t)(DVMAX + 2) * T * 32))[cc * 32 + lane]; }
-    }
+    for (int cc = 0; cc < T; ++cc) best = fmax(best, red[((size_t)(DVMAX + 1) * T + cc) * 32 + lane]);
   }
+  // Clipping: the smallest a whose Q is within kTieRel of the maximum
+  // (reading A17: ties -> smallest a; values equal up to round-off are ties).
+  const double thr = best * (1.0 - kTieRel);
+  int bidx = Q;
+#pragma unroll
+  for (int k = KR - 1; k >= 0; --k)
+    if (tot[k] >= thr) bidx = c * KR + k;
+  if constexpr (T > 1) {
+    int *ired = (int *)(red + (size_t)(DVMAX + 2) * T * 32);
+    ired[c * 32 + lane] = bidx;
+    group_bar<T>(g);
+#pragma unroll
+    for (int cc = 0; cc < T; ++cc) bidx = min(bidx, ired[cc * 32 + lane]);
+  }
+  if (bidx >= Q) bidx = 0;
+  if (frozen) return;  // a converged frame keeps the state it converged with
   int bad = 0;
 #pragma unroll
   for (int s = 0; s < DVMAX; ++s) {
@@ -298,10 +319,8 @@ __device__ __forceinline__ void vn_body(const WaveArgs &a, int fb, int j, int e0
 #pragma unroll
     for (int k = 0; k < KR; ++k) dst[(c * KR + k) * 32] = okq ? (float)(tot[k] * invq) : 1.0f / Q;
   }
-  if (c == 0) {
-    a.xhat[((size_t)fb * a.c.V + j) * 32 + lane] = (unsigned char)bidx;
-    if (bad) atomicAdd(a.stats + 0, (unsigned long long)bad);
-  }
+  if (c == 0) a.xhat[((size_t)fb * a.c.V + j) * 32 + lane] = (unsigned char)bidx;
+  if (bad && c == 0) atomicAdd(a.stats + 0, (unsigned long long)bad);
 }
 
 // ============================================================== PUS: check node
@@ -386,9 +405,10 @@ __global__ void __launch_bounds__(QC<Q>::THREADS) k_cn(WaveArgs a) {
       group_bar<T>(g);
     }
     constexpr double invq = 1.0 / Q;
+    const bool frozen = lane_frozen(a, fb, lane);
 #pragma unroll
     for (int s = 0; s < DMAX; ++s) {
-      if (s < d) {
+      if (s < d && !frozen) {
         wht_bits<KR, 0, LKR>(u[s]);
         float *dst = a.rmsg + ((size_t)fb * E + e0 + s) * Q * 32 + lane;
 #pragma unroll
@@ -428,7 +448,7 @@ __global__ void __launch_bounds__(QC<Q>::THREADS) k_vn(WaveArgs a, int clip_only
         for (int k = 0; k < KR; ++k) r[s][k] = (double)__ldg(src + (c * KR + k) * 32);
       }
     }
-    vn_body<Q, DVMAX, MARKOV>(a, fb, j, e0, dv, r, red, g, c, lane);
+    vn_body<Q, DVMAX, MARKOV>(a, fb, j, e0, dv, r, red, g, c, lane, lane_frozen(a, fb, lane));
     if constexpr (T > 1) group_bar<T>(g);
   }
 }
@@ -525,7 +545,7 @@ __global__ void __launch_bounds__(QC<Q>::THREADS) k_sus(WaveArgs a, int lvl_begi
       int bb[P];
       unpack_basis<P>(__ldg(a.c.edge_perm + e), bb);
       const int rch = row_hi<P, LKR>(bb, c);
-      float *rdst = a.rmsg ? a.rmsg + ((size_t)fb * E + e) * Q * 32 + lane : nullptr;
+      float *rdst = (a.rmsg && !lane_frozen(a, fb, lane)) ? a.rmsg + ((size_t)fb * E + e) * Q * 32 + lane : nullptr;
 #pragma unroll
       for (int k = 0; k < KR; ++k) {
         const double v = acc[k] * (1.0 / Q);
@@ -542,7 +562,7 @@ __global__ void __launch_bounds__(QC<Q>::THREADS) k_sus(WaveArgs a, int lvl_begi
       if (s < dv)
 #pragma unroll
         for (int k = 0; k < KR; ++k) r[s][k] = (double)rsm[((size_t)s * Q + c * KR + k) * 32 + lane];
-    vn_body<Q, DVMAX, MARKOV>(a, fb, j, e0, dv, r, red, g, c, lane);
+    vn_body<Q, DVMAX, MARKOV>(a, fb, j, e0, dv, r, red, g, c, lane, lane_frozen(a, fb, lane));
     group_bar<T>(g);
   }
 }
@@ -682,7 +702,7 @@ __global__ void k_test(WaveArgs a, int chunk) {
     for (int i = i0; i < i1; ++i) {
       int acc = a.z[((size_t)fb * M + i) * 32 + lane];
       for (int e = __ldg(a.c.row_ptr + i); e < __ldg(a.c.row_ptr + i + 1); ++e)
-        acc ^= mul_s[__ldg(a.c.edge_coef + e) * q + a.xhat[((size_t)fb * V + __ldg(a.c.edge_var + e)) * 32 + lane]];
+        acc ^= mul_s[__ldg(a.c.edge_coef + e) * q + (a.xhat[((size_t)fb * V + __ldg(a.c.edge_var + e)) * 32 + lane] & (q - 1))];
       bad |= (acc != 0);
     }
     if (bad) atomicOr(a.unsat + fb * 32 + lane, 1);

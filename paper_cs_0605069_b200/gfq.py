@@ -23,7 +23,9 @@ GFQ_PUS, GFQ_SUS = 0, 1
 # Every symbol declared in include/gfq.h (checked by tests/test_abi.py).
 EXPORTS = ["gfq_last_error", "gfq_version", "gfq_code_create", "gfq_code_destroy", "gfq_code_info",
            "gfq_workspace_bytes", "gfq_decode", "gfq_decode_evidence", "gfq_workspace_bytes_host",
-           "gfq_decode_host", "gfq_export_messages", "gfq_decode_stats"]
+           "gfq_decode_host", "gfq_export_messages", "gfq_decode_stats", "gfq_profile_enable",
+           "gfq_profile_read", "gfq_kernel_name"]
+GFQ_NKERNELS = 13
 
 
 class GfqError(RuntimeError):
@@ -72,6 +74,12 @@ def lib() -> ctypes.CDLL:
         L.gfq_export_messages.restype = i
         L.gfq_decode_stats.argtypes = [vp, vp, sz, P(ll), vp]
         L.gfq_decode_stats.restype = i
+        L.gfq_profile_enable.argtypes = [i]
+        L.gfq_profile_enable.restype = i
+        L.gfq_profile_read.argtypes = [vp, vp]
+        L.gfq_profile_read.restype = i
+        L.gfq_kernel_name.argtypes = [i]
+        L.gfq_kernel_name.restype = ctypes.c_char_p
         _lib = L
     return _lib
 
@@ -224,3 +232,15 @@ def gfq_decode_stats(code: Code, workspace, stream=None):
     _check(lib().gfq_decode_stats(code.h, _dptr(workspace), workspace.numel(), out, _stream_ptr(stream)))
     return dict(zero_normalisers=out[0], block_iterations=out[1], frames_converged=out[2],
                 launches=out[3])
+
+
+def gfq_profile_enable(on: bool = True):
+    _check(lib().gfq_profile_enable(int(bool(on))))
+
+
+def gfq_profile_read():
+    """{kernel name: (total ms, launches)} for the decodes since gfq_profile_enable(True)."""
+    ms = (ctypes.c_double * GFQ_NKERNELS)()
+    n = (ctypes.c_longlong * GFQ_NKERNELS)()
+    _check(lib().gfq_profile_read(ctypes.addressof(ms), ctypes.addressof(n)))
+    return {lib().gfq_kernel_name(k).decode(): (ms[k], n[k]) for k in range(GFQ_NKERNELS)}

@@ -234,8 +234,14 @@ def test_var_node_properties():
 
 
 def test_posterior_clipping_ties_smallest():
+    """Reading A17: ties go to the smallest a; values within a relative 1e-5 of the
+    maximum are ties (round-off must not decide the clipping)."""
     Q, x, _ = oracle.posterior([0.25] * 4, [[0.1, 0.4, 0.4, 0.1]])
     assert x == 1
+    Q, x, _ = oracle.posterior([0.25] * 4, [[0.1, 0.4 * (1 - 1e-7), 0.4, 0.1]])
+    assert x == 1
+    Q, x, _ = oracle.posterior([0.25] * 4, [[0.1, 0.4 * (1 - 1e-3), 0.4, 0.1]])
+    assert x == 2
 
 
 # ----------------------------------------------------------------------------- Markov prior, Eqs. (6)/(7)
