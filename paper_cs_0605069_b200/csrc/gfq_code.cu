@@ -131,6 +131,8 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
     std::vector<int> fill(col_ptr.begin(), col_ptr.end() - 1);
     for (long long e = 0; e < E; ++e) col_edge[fill[edge_var[e]]++] = (int)e;  // ascending check
   }
+  std::vector<int> edge_canon(E);
+  for (long long k = 0; k < E; ++k) edge_canon[col_edge[k]] = (int)k;
   int max_cdeg = 0, max_vdeg = 0;
   for (int i = 0; i < M; ++i) max_cdeg = std::max(max_cdeg, row_ptr[i + 1] - row_ptr[i]);
   for (int j = 0; j < V; ++j) max_vdeg = std::max(max_vdeg, col_ptr[j + 1] - col_ptr[j]);
@@ -177,6 +179,7 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   const size_t o_coef = off; off += al(E);
   const size_t o_col = off; off += al(sizeof(int) * (V + 1));
   const size_t o_cedge = off; off += al(sizeof(int) * E);
+  const size_t o_canon = off; off += al(sizeof(int) * E);
   const size_t o_lptr = off; off += al(sizeof(int) * (nlev + 1));
   const size_t o_lcol = off; off += al(sizeof(int) * V);
   const size_t o_mul = off; off += al((size_t)q * q);
@@ -189,6 +192,7 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   put(o_coef, edge_coef.data(), E);
   put(o_col, col_ptr.data(), sizeof(int) * (V + 1));
   put(o_cedge, col_edge.data(), sizeof(int) * E);
+  put(o_canon, edge_canon.data(), sizeof(int) * E);
   put(o_lptr, level_ptr.data(), sizeof(int) * (nlev + 1));
   put(o_lcol, level_cols.data(), sizeof(int) * V);
   put(o_mul, mul.data(), (size_t)q * q);
@@ -218,6 +222,7 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   c->d.edge_coef = b + o_coef;
   c->d.col_ptr = (const int *)(b + o_col);
   c->d.col_edge = (const int *)(b + o_cedge);
+  c->d.edge_canon = (const int *)(b + o_canon);
   c->d.level_ptr = (const int *)(b + o_lptr);
   c->d.level_cols = (const int *)(b + o_lcol);
   c->d.mul = b + o_mul;

@@ -33,6 +33,7 @@ struct DevCode {
   const unsigned char *edge_coef;       // [E] h_e
   const int *col_ptr;        // [V+1]
   const int *col_edge;       // [E]     edges of variable j (ascending check) == canonical order
+  const int *edge_canon;     // [E]     canonical (variable-major) position of edge e
   const int *level_ptr;      // [L+1]   SUS dependency levels
   const int *level_cols;     // [V]
   const unsigned char *mul;  // [q*q]   GF(2^p) product table
