@@ -55,10 +55,22 @@ struct QC {
   static_assert(KR >= 2 && KR <= Q && (Q % KR) == 0, "bad KR");
 };
 
-// entries per thread by field size (tuning knob)
-template <int Q>
+// entries per thread by field size and kernel (tuning knobs)
+#ifndef GFQ_KR_CN16
+#define GFQ_KR_CN16 16
+#endif
+#ifndef GFQ_KR_VN16
+#define GFQ_KR_VN16 16
+#endif
+#ifndef GFQ_KR_SUS16
+#define GFQ_KR_SUS16 8
+#endif
+enum KernelKind { KCN, KVN, KSUS };
+template <int Q, int K>
 struct KRof {
-  static constexpr int v = Q <= 8 ? Q : 8;
+  static constexpr int v = Q <= 8 ? Q
+                           : Q == 16 ? (K == KCN ? GFQ_KR_CN16 : K == KVN ? GFQ_KR_VN16 : GFQ_KR_SUS16)
+                                     : 8;
 };
 // largest stage count in [2, max_s] such that the CTA fits the 227 KB of
 // dynamic shared memory (per_stage and other are bytes per CTA)
@@ -211,6 +223,47 @@ __device__ __forceinline__ void leave_one_out(double (&u)[DM][KR], int d) {
   }
 }
 
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// A consumer warp is done reading a stage: one arrival per warp on its
+// "empty" barrier (count T) lets the producer refill it.
+__device__ __forceinline__ void release_stage(uint64_t *empty, int lane) {
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty);
+}
+
+// Contiguous share [lo, hi) of ntask tasks for global group gg of ngroups.
+__device__ __forceinline__ void group_range(long long ntask, long long gg, long long ngroups, long long &lo,
+                                            long long &hi) {
+  const long long chunk = (ntask + ngroups - 1) / ngroups;
+  lo = gg * chunk;
+  hi = lo + chunk < ntask ? lo + chunk : ntask;
+  if (lo > ntask) lo = ntask;
+}
+
+// Stage header written by the producer (plain shared store, published by the
+// mbarrier arrive): task coordinates.
+struct __align__(16) TaskInfo {
+  int fb, item, e0, deg;  // block, check/variable, first edge, degree
+  int s, r0, d, pos;      // SUS unit: check slot, check row start / degree, position of e
+  int i, pad0, pad1, pad2;
+};
+
 // ============================================================== priors
 // Extra rows a variable task needs besides its r messages, fetched into the
 // stage after them: noise symbol -> its p per-bit flip probabilities; Markov
@@ -222,32 +275,24 @@ struct Extra {
 };
 
 template <int Q, bool MARKOV>
-__device__ __forceinline__ uint32_t issue_extras(const WaveArgs &a, int fb, int j, float *dst,
-                                                 const float *(&src)[2], uint32_t (&nb)[2],
-                                                 float *(&dsts)[2]) {
+__device__ __forceinline__ uint32_t extras_bytes(const WaveArgs &a, int j) {
   constexpr int P = ilog2(Q);
   const int N = a.c.N;
-  uint32_t total = 0;
-  nb[0] = nb[1] = 0;
+  if (j >= N) return P * 128;
+  if (MARKOV && a.t > 1 && a.qs_old) return (uint32_t)((j > 0) + (j < N - 1)) * Q * 128;
+  return 0;
+}
+
+template <int Q, bool MARKOV>
+__device__ __forceinline__ void issue_extras(const WaveArgs &a, int fb, int j, unsigned char *dst, uint64_t *bar) {
+  constexpr int P = ilog2(Q);
+  const int N = a.c.N;
   if (j >= N) {
-    src[0] = a.pi + ((size_t)fb * a.c.M * P + (size_t)(j - N) * P) * 32;
-    dsts[0] = dst;
-    nb[0] = P * 128;
-    total = nb[0];
+    bulk_g2s(dst, a.pi + ((size_t)fb * a.c.M * P + (size_t)(j - N) * P) * 32, P * 128, bar);
   } else if (MARKOV && a.t > 1 && a.qs_old) {
-    if (j > 0) {
-      src[0] = a.qs_old + ((size_t)fb * N + (j - 1)) * Q * 32;
-      dsts[0] = dst;
-      nb[0] = Q * 128;
-    }
-    if (j < N - 1) {
-      src[1] = a.qs_old + ((size_t)fb * N + (j + 1)) * Q * 32;
-      dsts[1] = dst + Q * 32;
-      nb[1] = Q * 128;
-    }
-    total = nb[0] + nb[1];
+    if (j > 0) bulk_g2s(dst, a.qs_old + ((size_t)fb * N + (j - 1)) * Q * 32, Q * 128, bar);
+    if (j < N - 1) bulk_g2s(dst + Q * 128, a.qs_old + ((size_t)fb * N + (j + 1)) * Q * 32, Q * 128, bar);
   }
-  return total;
 }
 
 // Prior p_j^a for the KR entries a = c*KR + k (layout A) of this thread, from
@@ -285,12 +330,14 @@ __device__ __forceinline__ void prior_from(const WaveArgs &a, int j, int c, int 
     return;
   }
   double L[KR], R[KR];
+  const float *exl = ex;
+  const float *exr = ex + (j > 0 ? Q * 32 : 0);
   if (j > 0) {
 #pragma unroll
     for (int k = 0; k < KR; ++k) L[k] = 0.0;
 #pragma unroll 4
     for (int x = 0; x < Q; ++x) {
-      const double qv = (double)ex[x * 32 + lane];
+      const double qv = (double)exl[x * 32 + lane];
 #pragma unroll
       for (int k = 0; k < KR; ++k) L[k] += qv * __ldg(a.T + x * Q + c * KR + k);
     }
@@ -303,7 +350,7 @@ __device__ __forceinline__ void prior_from(const WaveArgs &a, int j, int c, int 
     for (int k = 0; k < KR; ++k) R[k] = 0.0;
 #pragma unroll 4
     for (int x = 0; x < Q; ++x) {
-      const double qv = (double)ex[(Q + x) * 32 + lane];
+      const double qv = (double)exr[x * 32 + lane];
 #pragma unroll
       for (int k = 0; k < KR; ++k) R[k] += __ldg(a.T + (c * KR + k) * Q + x) * qv;
     }
@@ -319,11 +366,11 @@ __device__ __forceinline__ void prior_from(const WaveArgs &a, int j, int c, int 
 // Eq. (4): q_ij^a = alpha_ij p_j^a prod_{i' != i} r_i'j^a, and
 // Eq. (5): Q_j^a = alpha_j p_j^a prod_i r_ij^a, clipped to the
 // smallest a within kTieRel of the maximum (reading A17).  r[s][k] holds r of
-// check slot s at a = c*KR + k; pr the prior.  Writes the dv q messages (to
-// their check-major slots), x_hat, the Markov snapshot and (keep) Q.
-// red: group scratch of (DVMAX+3)*T*32 doubles.
+// check slot s at a = c*KR + k; pr the prior; qdst[s] the check-major id of
+// the edge of slot s.  Writes the dv q messages, x_hat, the Markov snapshot
+// and (keep) Q.  red: group scratch of (DVMAX+3)*T*32 doubles.
 template <int Q, int KR, int DVMAX, bool MARKOV>
-__device__ __forceinline__ void vn_body(const WaveArgs &a, int fb, int j, int e0, int dv,
+__device__ __forceinline__ void vn_body(const WaveArgs &a, int fb, int j, int dv, const int (&qdst)[DVMAX],
                                         double (&r)[DVMAX][KR], const double (&pr)[KR], double *red,
                                         int g, int c, int lane, bool frozen) {
   constexpr int T = Q / KR;
@@ -390,8 +437,7 @@ __device__ __forceinline__ void vn_body(const WaveArgs &a, int fb, int j, int e0
 #pragma unroll
   for (int s = 0; s < DVMAX; ++s) {
     if (s < dv) {
-      const int e = __ldg(a.c.col_edge + e0 + s);
-      float *dst = a.qmsg + ((size_t)fb * E + e) * Q * 32 + lane;
+      float *dst = a.qmsg + ((size_t)fb * E + qdst[s]) * Q * 32 + lane;
       const double sm = sums[s];
       const bool ok = sm > 0.0 && isfinite(sm);
       bad += !ok;
@@ -419,28 +465,74 @@ __device__ __forceinline__ void vn_body(const WaveArgs &a, int fb, int j, int e0
   if (bad && c == 0) atomicAdd(a.stats + 0, (unsigned long long)bad);
 }
 
-// ============================================================== PUS: check node
+// ============================================================== pipeline shapes
+// CTA = 1 producer warp (lane 0 issues every TMA copy) + G groups of T
+// consumer warps.  Group g owns a ring of S stages with "full" (TMA bytes
+// landed) and "empty" (all T warps done reading) mbarriers.
+//   stage = [TaskInfo 64B][static desc 64..128B][z 32B -> 128][conv 128B][payload]
+constexpr int kHdr = 512;  // stage header bytes (payload offset)
+
 template <int Q, int KR, int DMAX, int S, int G>
 struct CNShape {
   static constexpr int T = Q / KR;
-  static constexpr size_t STAGE_F = (size_t)DMAX * Q * 32;
-  static constexpr size_t XP_D = T > 1 ? (size_t)DMAX * Q * 32 : 0;
-  static constexpr size_t GROUP_BYTES = 128 + S * STAGE_F * 4 + XP_D * 8;
-  static constexpr size_t SMEM = G * GROUP_BYTES;
-  static constexpr int THREADS = G * T * 32;
+  static constexpr size_t STAGE_B = kHdr + (size_t)DMAX * Q * 128;
+  static constexpr size_t SCR_B = T > 1 ? (size_t)DMAX * Q * 32 * 8 : 0;
+  static constexpr size_t BARS_B = ((16 * S * G + 127) / 128) * 128;
+  static constexpr size_t SMEM = BARS_B + (size_t)G * S * STAGE_B + (size_t)G * SCR_B;
+  static constexpr int THREADS = (1 + G * T) * 32;
 };
 
-template <int Q>
-__device__ __forceinline__ void cn_issue(const WaveArgs &a, long long task, long long ntask, float *dst,
-                                         uint64_t *bar) {
-  if (task >= ntask) return;
+template <int Q, int KR, int DVMAX, bool MARKOV, int S, int G>
+struct VNShape {
+  static constexpr int T = Q / KR;
+  static constexpr int XR = Extra<Q, MARKOV>::rows;
+  static constexpr size_t STAGE_B = kHdr + ((size_t)DVMAX * Q + XR) * 128;
+  static constexpr size_t SCR_B = (size_t)(DVMAX + 3) * T * 32 * 8;
+  static constexpr size_t BARS_B = ((16 * S * G + 127) / 128) * 128;
+  static constexpr size_t SMEM = BARS_B + (size_t)G * S * STAGE_B + (size_t)G * SCR_B;
+  static constexpr int THREADS = (1 + G * T) * 32;
+};
+
+template <int Q, int KR, int DMAX, int DVMAX, bool MARKOV, int S, int G>
+struct SUSShape {
+  static constexpr int T = Q / KR;
+  static constexpr int XR = Extra<Q, MARKOV>::rows;
+  static constexpr size_t STAGE_B = kHdr + ((size_t)(DMAX - 1) * Q + XR) * 128;
+  static constexpr size_t FWD_D = T > 1 ? (size_t)(DMAX - 1) * Q * 32 : 0;
+  static constexpr size_t ACC_D = T > 1 ? (size_t)Q * 32 : 0;
+  static constexpr size_t RED_D = (size_t)(DVMAX + 3) * T * 32;
+  static constexpr size_t RSM_F = (size_t)DVMAX * Q * 32;
+  static constexpr size_t SCR_B = (FWD_D + ACC_D + RED_D) * 8 + RSM_F * 4;
+  static constexpr size_t BARS_B = ((16 * S * G + 127) / 128) * 128;
+  static constexpr size_t SMEM = BARS_B + (size_t)G * S * STAGE_B + (size_t)G * SCR_B;
+  static constexpr int THREADS = (1 + G * T) * 32;
+};
+
+template <int S, int G>
+__device__ __forceinline__ void init_bars(uint64_t *bars, int T) {
+  // bars[0 .. G*S): full (1 arrival + tx bytes), bars[G*S .. 2*G*S): empty (T arrivals)
+  for (int k = 0; k < G * S; ++k) {
+    mbar_init(bars + k, 1);
+    mbar_init(bars + G * S + k, (uint32_t)T);
+  }
+  fence_mbar_init();
+}
+
+// ============================================================== PUS: check node
+template <int Q, int DMAX>
+__device__ __forceinline__ void cn_issue(const WaveArgs &a, long long task, unsigned char *sb, uint64_t *full) {
   const int M = a.c.M;
   const int fb = a.list[task / M];
   const int i = (int)(task % M);
   const int e0 = __ldg(a.c.row_ptr + i), d = __ldg(a.c.row_ptr + i + 1) - e0;
-  const uint32_t bytes = (uint32_t)d * Q * 128;
-  mbar_expect_tx(bar, bytes);
-  if (bytes) bulk_g2s(dst, a.qmsg + ((size_t)fb * a.c.E + e0) * Q * 32, bytes, bar);
+  TaskInfo *ti = (TaskInfo *)sb;
+  ti->fb = fb; ti->item = i; ti->e0 = e0; ti->deg = d;
+  const uint32_t msg = (uint32_t)d * Q * 128;
+  mbar_expect_tx(full, 128 + 32 + (a.early_exit ? 128 : 0) + msg);
+  bulk_g2s(sb + 128, a.c.check_desc + i, 128, full);
+  bulk_g2s(sb + 256, a.z + ((size_t)fb * M + i) * 32, 32, full);
+  if (a.early_exit) bulk_g2s(sb + 384, a.conv + fb * 32, 128, full);
+  if (msg) bulk_g2s(sb + kHdr, a.qmsg + ((size_t)fb * a.c.E + e0) * Q * 32, msg, full);
 }
 
 // Eq. (3) for every edge of check i (horizontal pass),
@@ -455,55 +547,72 @@ __global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(Wave
   using C = QC<Q, KR>;
   constexpr int T = C::T, LKR = C::LKR, LT = C::LT, P = C::P;
   extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *bars = (uint64_t *)smem;
+  unsigned char *stages = smem + Sh::BARS_B;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = warp / T, c = warp % T;
-  unsigned char *gb = smem + (size_t)g * Sh::GROUP_BYTES;
-  uint64_t *bars = (uint64_t *)gb;
-  float *stg = (float *)(gb + 128);
-  double *xp = (double *)(gb + 128 + S * Sh::STAGE_F * 4);
-  const bool producer = (c == 0) && (lane == 0);
-  if (producer) {
-#pragma unroll
-    for (int s = 0; s < S; ++s) mbar_init(bars + s, 1);
-    fence_mbar_init();
-  }
+  if (threadIdx.x == 0) init_bars<S, G>(bars, T);
   __syncthreads();
   const int M = a.c.M;
   const long long E = a.c.E;
   const long long ntask = (long long)(*a.nactive) * M;
-  const long long first = (long long)blockIdx.x * G + g, stride = (long long)gridDim.x * G;
-  if (producer) {
+  const long long ngroups = (long long)gridDim.x * G;
+  if (warp == 0) {  // ---------------- producer
+    if (lane != 0) return;
+    long long t[G], hi[G];
+    int ring[G];
 #pragma unroll
-    for (int n = 0; n < S; ++n) cn_issue<Q>(a, first + n * stride, ntask, stg + n * Sh::STAGE_F, bars + n);
-  }
-  for (long long n = 0;; ++n) {
-    const long long task = first + n * stride;
-    if (task >= ntask) break;
-    const int st = (int)(n % S);
-    const int fb = a.list[task / M];
-    const int i = (int)(task % M);
-    const int e0 = __ldg(a.c.row_ptr + i), d = __ldg(a.c.row_ptr + i + 1) - e0;
-    const int z = a.z[((size_t)fb * M + i) * 32 + lane];
-    int bb[DMAX][P];
-    int rc[DMAX];
+    for (int g = 0; g < G; ++g) {
+      group_range(ntask, (long long)blockIdx.x * G + g, ngroups, t[g], hi[g]);
+      ring[g] = 0;
+    }
+    for (bool any = true; any;) {
+      any = false;
 #pragma unroll
-    for (int s = 0; s < DMAX; ++s) {
-      if (s < d) {
-        unpack_basis<P>(__ldg(a.c.edge_perm + e0 + s), bb[s]);
-        rc[s] = row_hi<P, LKR>(bb[s], c);
+      for (int g = 0; g < G; ++g) {
+        if (t[g] >= hi[g]) continue;
+        any = true;
+        const int st = ring[g] % S, u = ring[g] / S;
+        if (u > 0 && !mbar_test(bars + G * S + g * S + st, (u - 1) & 1)) continue;
+        cn_issue<Q, DMAX>(a, t[g], stages + (size_t)(g * S + st) * Sh::STAGE_B, bars + g * S + st);
+        ++t[g];
+        ++ring[g];
       }
     }
-    mbar_wait(bars + st, (uint32_t)((n / S) & 1));
-    const float *in = stg + st * Sh::STAGE_F + lane;
+    return;
+  }
+  // ---------------- consumers
+  const int cw = warp - 1, g = cw / T, c = cw % T;
+  double *xp = (double *)(stages + (size_t)G * S * Sh::STAGE_B + (size_t)g * Sh::SCR_B);
+  long long lo, hi;
+  group_range(ntask, (long long)blockIdx.x * G + g, ngroups, lo, hi);
+  for (long long task = lo; task < hi; ++task) {
+    const int rr = (int)(task - lo), st = rr % S;
+    unsigned char *sb = stages + (size_t)(g * S + st) * Sh::STAGE_B;
+    mbar_wait(bars + g * S + st, (uint32_t)((rr / S) & 1));
+    const TaskInfo ti = *(const TaskInfo *)sb;
+    const CheckDesc *cd = (const CheckDesc *)(sb + 128);
+    const int fb = ti.fb, d = ti.deg;
+    const int z = sb[256 + lane];
+    const bool frozen = a.early_exit && ((const int *)(sb + 384))[lane] != 0;
+    const float *in = (const float *)(sb + kHdr) + lane;
+    int bb[DMAX][P];
+    int rc[DMAX];
+    int canon[DMAX];
     double u[DMAX][KR];
 #pragma unroll
     for (int s = 0; s < DMAX; ++s) {
       if (s < d) {
+        unpack_basis<P>(cd->perm[s], bb[s]);
+        canon[s] = cd->canon[s];
+        rc[s] = row_hi<P, LKR>(bb[s], c);
 #pragma unroll
         for (int k = 0; k < KR; ++k) u[s][k] = (double)in[(s * Q + (rc[s] ^ row_lo<P, LKR>(bb[s], k))) * 32];
-        wht_bits<KR, 0, LKR>(u[s]);
       }
     }
+    release_stage(bars + G * S + g * S + st, lane);
+#pragma unroll
+    for (int s = 0; s < DMAX; ++s)
+      if (s < d) wht_bits<KR, 0, LKR>(u[s]);
     if constexpr (T > 1) {
 #pragma unroll
       for (int s = 0; s < DMAX; ++s)
@@ -511,8 +620,6 @@ __global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(Wave
 #pragma unroll
           for (int k = 0; k < KR; ++k) xp[((size_t)s * Q + c * KR + k) * 32 + lane] = u[s][k];
       group_bar<T>(g);
-      // every warp of the group has read its rows of stage st: refill it
-      if (producer) cn_issue<Q>(a, task + S * stride, ntask, stg + st * Sh::STAGE_F, bars + st);
 #pragma unroll
       for (int s = 0; s < DMAX; ++s)
         if (s < d) {
@@ -520,9 +627,6 @@ __global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(Wave
           for (int k = 0; k < KR; ++k) u[s][k] = xp[((size_t)s * Q + k * T + c) * 32 + lane];
           wht_bits<KR, LKR - LT, LKR>(u[s]);
         }
-    } else {
-      __syncwarp();
-      if (producer) cn_issue<Q>(a, task + S * stride, ntask, stg + st * Sh::STAGE_F, bars + st);
     }
     leave_one_out<DMAX, KR>(u, d);
 #pragma unroll
@@ -552,13 +656,12 @@ __global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(Wave
       group_bar<T>(g);
     }
     constexpr double invq = 1.0 / Q;
-    const bool frozen = lane_frozen(a, fb, lane);
 #pragma unroll
     for (int s = 0; s < DMAX; ++s) {
       if (s < d) {
         wht_bits<KR, 0, LKR>(u[s]);
         if (!frozen) {
-          float *dst = a.rmsg + ((size_t)fb * E + __ldg(a.c.edge_canon + e0 + s)) * Q * 32 + lane;
+          float *dst = a.rmsg + ((size_t)fb * E + canon[s]) * Q * 32 + lane;
 #pragma unroll
           for (int k = 0; k < KR; ++k) {
             const double v = u[s][k] * invq;
@@ -571,35 +674,22 @@ __global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(Wave
 }
 
 // ============================================================== PUS: variable node
-template <int Q, int KR, int DVMAX, bool MARKOV, int S, int G>
-struct VNShape {
-  static constexpr int T = Q / KR;
-  static constexpr int XR = Extra<Q, MARKOV>::rows;
-  static constexpr size_t STAGE_F = ((size_t)DVMAX * Q + XR) * 32;
-  static constexpr size_t RED_D = (size_t)(DVMAX + 3) * T * 32;
-  static constexpr size_t GROUP_BYTES = 128 + S * STAGE_F * 4 + RED_D * 8;
-  static constexpr size_t SMEM = G * GROUP_BYTES;
-  static constexpr int THREADS = G * T * 32;
-};
-
 template <int Q, int DVMAX, bool MARKOV>
-__device__ __forceinline__ void vn_issue(const WaveArgs &a, long long task, long long ntask, float *dst,
-                                         uint64_t *bar, int clip_only) {
-  if (task >= ntask) return;
+__device__ __forceinline__ void vn_issue(const WaveArgs &a, long long task, unsigned char *sb, uint64_t *full,
+                                         int clip_only) {
   const int V = a.c.V;
   const int fb = a.list[task / V];
   const int j = (int)(task % V);
   const int e0 = __ldg(a.c.col_ptr + j);
   const int dv = clip_only ? 0 : __ldg(a.c.col_ptr + j + 1) - e0;
+  TaskInfo *ti = (TaskInfo *)sb;
+  ti->fb = fb; ti->item = j; ti->e0 = e0; ti->deg = dv;
   const uint32_t br = (uint32_t)dv * Q * 128;
-  const float *xs[2] = {nullptr, nullptr};
-  float *xd[2] = {nullptr, nullptr};
-  uint32_t xb[2];
-  const uint32_t bx = issue_extras<Q, MARKOV>(a, fb, j, dst + (size_t)DVMAX * Q * 32, xs, xb, xd);
-  mbar_expect_tx(bar, br + bx);
-  if (br) bulk_g2s(dst, a.rmsg + ((size_t)fb * a.c.E + e0) * Q * 32, br, bar);  // canonical order
-  if (xb[0]) bulk_g2s(xd[0], xs[0], xb[0], bar);
-  if (xb[1]) bulk_g2s(xd[1], xs[1], xb[1], bar);
+  mbar_expect_tx(full, 64 + (a.early_exit ? 128 : 0) + br + extras_bytes<Q, MARKOV>(a, j));
+  bulk_g2s(sb + 128, a.c.var_desc + j, 64, full);
+  if (a.early_exit) bulk_g2s(sb + 384, a.conv + fb * 32, 128, full);
+  if (br) bulk_g2s(sb + kHdr, a.rmsg + ((size_t)fb * a.c.E + e0) * Q * 32, br, full);  // canonical order
+  issue_extras<Q, MARKOV>(a, fb, j, sb + kHdr + (size_t)DVMAX * Q * 128, full);
 }
 
 template <int Q, int KR, int DVMAX, bool MARKOV, int S, int G>
@@ -608,115 +698,103 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
   using Sh = VNShape<Q, KR, DVMAX, MARKOV, S, G>;
   constexpr int T = Sh::T;
   extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *bars = (uint64_t *)smem;
+  unsigned char *stages = smem + Sh::BARS_B;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = warp / T, c = warp % T;
-  unsigned char *gb = smem + (size_t)g * Sh::GROUP_BYTES;
-  uint64_t *bars = (uint64_t *)gb;
-  float *stg = (float *)(gb + 128);
-  double *red = (double *)(gb + 128 + S * Sh::STAGE_F * 4);
-  const bool producer = (c == 0) && (lane == 0);
-  if (producer) {
-#pragma unroll
-    for (int s = 0; s < S; ++s) mbar_init(bars + s, 1);
-    fence_mbar_init();
-  }
+  if (threadIdx.x == 0) init_bars<S, G>(bars, T);
   __syncthreads();
   const int V = a.c.V;
   const long long ntask = (long long)(*a.nactive) * V;
-  const long long first = (long long)blockIdx.x * G + g, stride = (long long)gridDim.x * G;
-  if (producer) {
+  const long long ngroups = (long long)gridDim.x * G;
+  if (warp == 0) {  // ---------------- producer
+    if (lane != 0) return;
+    long long t[G], hi[G];
+    int ring[G];
 #pragma unroll
-    for (int n = 0; n < S; ++n)
-      vn_issue<Q, DVMAX, MARKOV>(a, first + n * stride, ntask, stg + n * Sh::STAGE_F, bars + n, clip_only);
+    for (int g = 0; g < G; ++g) {
+      group_range(ntask, (long long)blockIdx.x * G + g, ngroups, t[g], hi[g]);
+      ring[g] = 0;
+    }
+    for (bool any = true; any;) {
+      any = false;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (t[g] >= hi[g]) continue;
+        any = true;
+        const int st = ring[g] % S, u = ring[g] / S;
+        if (u > 0 && !mbar_test(bars + G * S + g * S + st, (u - 1) & 1)) continue;
+        vn_issue<Q, DVMAX, MARKOV>(a, t[g], stages + (size_t)(g * S + st) * Sh::STAGE_B, bars + g * S + st,
+                                   clip_only);
+        ++t[g];
+        ++ring[g];
+      }
+    }
+    return;
   }
-  for (long long n = 0;; ++n) {
-    const long long task = first + n * stride;
-    if (task >= ntask) break;
-    const int st = (int)(n % S);
-    const int fb = a.list[task / V];
-    const int j = (int)(task % V);
-    const int e0 = __ldg(a.c.col_ptr + j);
-    const int dv = clip_only ? 0 : __ldg(a.c.col_ptr + j + 1) - e0;
-    const bool frozen = lane_frozen(a, fb, lane);
-    mbar_wait(bars + st, (uint32_t)((n / S) & 1));
-    const float *in = stg + st * Sh::STAGE_F;
+  const int cw = warp - 1, g = cw / T, c = cw % T;
+  double *red = (double *)(stages + (size_t)G * S * Sh::STAGE_B + (size_t)g * Sh::SCR_B);
+  long long lo, hi;
+  group_range(ntask, (long long)blockIdx.x * G + g, ngroups, lo, hi);
+  for (long long task = lo; task < hi; ++task) {
+    const int rr = (int)(task - lo), st = rr % S;
+    unsigned char *sb = stages + (size_t)(g * S + st) * Sh::STAGE_B;
+    mbar_wait(bars + g * S + st, (uint32_t)((rr / S) & 1));
+    const TaskInfo ti = *(const TaskInfo *)sb;
+    const VarDesc *vd = (const VarDesc *)(sb + 128);
+    const int fb = ti.fb, j = ti.item, dv = ti.deg;
+    const bool frozen = a.early_exit && ((const int *)(sb + 384))[lane] != 0;
+    const float *in = (const float *)(sb + kHdr);
+    int qdst[DVMAX];
     double r[DVMAX][KR];
 #pragma unroll
     for (int s = 0; s < DVMAX; ++s)
-      if (s < dv)
+      if (s < dv) {
+        qdst[s] = vd->qdst[s];
 #pragma unroll
         for (int k = 0; k < KR; ++k) r[s][k] = (double)in[(s * Q + c * KR + k) * 32 + lane];
+      }
     double pr[KR];
     prior_from<Q, KR, MARKOV>(a, j, c, lane, in + (size_t)DVMAX * Q * 32, pr);
-    group_bar<T>(g);  // stage st fully read by the group
-    if (producer)
-      vn_issue<Q, DVMAX, MARKOV>(a, task + S * stride, ntask, stg + st * Sh::STAGE_F, bars + st, clip_only);
-    vn_body<Q, KR, DVMAX, MARKOV>(a, fb, j, e0, dv, r, pr, red, g, c, lane, frozen);
+    release_stage(bars + G * S + g * S + st, lane);
+    vn_body<Q, KR, DVMAX, MARKOV>(a, fb, j, dv, qdst, r, pr, red, g, c, lane, frozen);
     if constexpr (T > 1) group_bar<T>(g);  // red reusable
   }
 }
 
 // ============================================================== SUS: one dependency level
-template <int Q, int KR, int DMAX, int DVMAX, bool MARKOV, int S, int G>
-struct SUSShape {
-  static constexpr int T = Q / KR;
-  static constexpr int XR = Extra<Q, MARKOV>::rows;
-  static constexpr size_t STAGE_F = ((size_t)(DMAX - 1) * Q + XR) * 32;
-  static constexpr size_t FWD_D = T > 1 ? (size_t)(DMAX - 1) * Q * 32 : 0;
-  static constexpr size_t ACC_D = T > 1 ? (size_t)Q * 32 : 0;
-  static constexpr size_t RED_D = (size_t)(DVMAX + 3) * T * 32;
-  static constexpr size_t RSM_F = (size_t)DVMAX * Q * 32;
-  static constexpr size_t GROUP_BYTES = 128 + S * STAGE_F * 4 + FWD_D * 8 + ACC_D * 8 + RED_D * 8 + RSM_F * 4;
-  static constexpr size_t SMEM = G * GROUP_BYTES;
-  static constexpr int THREADS = G * T * 32;
-};
-
-// Producer cursor over SUS "units": one unit = one check of one column
-// (its other edges, in at most two contiguous runs); the last unit of a
-// column also carries the prior's extra rows.
-struct SusCursor {
-  long long n;  // task index of this group
-  int s;        // check slot within the column
-};
-
+// Units: one per (column, check slot) -- the check's other edges in at most
+// two contiguous runs; the last unit of a column also carries the prior's
+// extra rows and the column's VarDesc.
 template <int Q, int DMAX, bool MARKOV>
-__device__ __forceinline__ void sus_issue(const WaveArgs &a, SusCursor &cur, long long first, long long stride,
-                                          long long ntask, int lvl_begin, int ncols, float *dst,
-                                          uint64_t *bar) {
-  const long long task = first + cur.n * stride;
-  if (task >= ntask) return;
+__device__ __forceinline__ void sus_issue(const WaveArgs &a, long long task, int s, int lvl_begin, int ncols,
+                                          unsigned char *sb, uint64_t *full, int &nunits_out) {
   const int fb = a.list[task / ncols];
-  const int j = __ldg(a.c.level_cols + lvl_begin + (int)(task % ncols));
-  const int e0 = __ldg(a.c.col_ptr + j), dv = __ldg(a.c.col_ptr + j + 1) - e0;
-  const int nunits = dv > 0 ? dv : 1;
-  const int s = cur.s;
-  const float *src0 = nullptr, *src1 = nullptr;
+  const LvlCol lc = a.c.lvl_col[lvl_begin + (int)(task % ncols)];
+  const int nunits = lc.dv > 0 ? lc.dv : 1;
+  nunits_out = nunits;
+  const LvlUnit un = a.c.lvl_unit[lc.unit0 + s];
+  TaskInfo *ti = (TaskInfo *)sb;
+  ti->fb = fb; ti->item = lc.j; ti->e0 = lc.e0; ti->deg = lc.dv;
+  ti->s = s; ti->r0 = un.r0; ti->d = un.d; ti->pos = un.pos; ti->i = un.i;
+  const bool last = (s == nunits - 1);
   uint32_t b0 = 0, b1 = 0;
-  int pos = 0;
-  if (dv > 0) {
-    const int e = __ldg(a.c.col_edge + e0 + s);
-    const int i = __ldg(a.c.edge_check + e);
-    const int r0 = __ldg(a.c.row_ptr + i), d = __ldg(a.c.row_ptr + i + 1) - r0;
-    pos = e - r0;
-    const float *rowbase = a.qmsg + ((size_t)fb * a.c.E + r0) * Q * 32;
-    src0 = rowbase;
-    b0 = (uint32_t)pos * Q * 128;
-    src1 = rowbase + (size_t)(pos + 1) * Q * 32;
-    b1 = (uint32_t)(d - 1 - pos) * Q * 128;
+  const float *rowbase = a.qmsg + ((size_t)fb * a.c.E + un.r0) * Q * 32;
+  if (lc.dv > 0) {
+    b0 = (uint32_t)un.pos * Q * 128;
+    b1 = (uint32_t)(un.d - 1 - un.pos) * Q * 128;
   }
-  const float *xs[2] = {nullptr, nullptr};
-  float *xd[2] = {nullptr, nullptr};
-  uint32_t xb[2] = {0, 0};
-  uint32_t bx = 0;
-  if (s == nunits - 1) bx = issue_extras<Q, MARKOV>(a, fb, j, dst + (size_t)(DMAX - 1) * Q * 32, xs, xb, xd);
-  mbar_expect_tx(bar, b0 + b1 + bx);
-  if (b0) bulk_g2s(dst, src0, b0, bar);
-  if (b1) bulk_g2s(dst + (size_t)pos * Q * 32, src1, b1, bar);
-  if (xb[0]) bulk_g2s(xd[0], xs[0], xb[0], bar);
-  if (xb[1]) bulk_g2s(xd[1], xs[1], xb[1], bar);
-  if (++cur.s == nunits) {
-    cur.s = 0;
-    ++cur.n;
+  const uint32_t bx = last ? 64 + extras_bytes<Q, MARKOV>(a, lc.j) : 0;
+  mbar_expect_tx(full, (lc.dv > 0 ? 64 + 32 : 0) + (a.early_exit ? 128 : 0) + b0 + b1 + bx);
+  if (lc.dv > 0) {
+    bulk_g2s(sb + 128, a.c.sus_desc + lc.e0 + s, 64, full);
+    bulk_g2s(sb + 256, a.z + ((size_t)fb * a.c.M + un.i) * 32, 32, full);
+  }
+  if (a.early_exit) bulk_g2s(sb + 384, a.conv + fb * 32, 128, full);
+  if (b0) bulk_g2s(sb + kHdr, rowbase, b0, full);
+  if (b1) bulk_g2s(sb + kHdr + (size_t)un.pos * Q * 128, rowbase + (size_t)(un.pos + 1) * Q * 32, b1, full);
+  if (last) {
+    bulk_g2s(sb + 192, a.c.var_desc + lc.j, 64, full);
+    issue_extras<Q, MARKOV>(a, fb, lc.j, sb + kHdr + (size_t)(DMAX - 1) * Q * 128, full);
   }
 }
 
@@ -734,65 +812,88 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
   constexpr int T = C::T, LKR = C::LKR, LT = C::LT, P = C::P;
   constexpr int DO = DMAX - 1;
   extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *bars = (uint64_t *)smem;
+  unsigned char *stages = smem + Sh::BARS_B;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = warp / T, c = warp % T;
-  unsigned char *gb = smem + (size_t)g * Sh::GROUP_BYTES;
-  uint64_t *bars = (uint64_t *)gb;
-  float *stg = (float *)(gb + 128);
-  double *fwd = (double *)(gb + 128 + S * Sh::STAGE_F * 4);
+  if (threadIdx.x == 0) init_bars<S, G>(bars, T);
+  __syncthreads();
+  const long long E = a.c.E;
+  const long long ntask = (long long)(*a.nactive) * ncols;
+  const long long ngroups = (long long)gridDim.x * G;
+  if (warp == 0) {  // ---------------- producer: walks (task, unit) per group
+    if (lane != 0) return;
+    long long t[G], hi[G];
+    int ring[G], su[G], nu[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      group_range(ntask, (long long)blockIdx.x * G + g, ngroups, t[g], hi[g]);
+      ring[g] = 0;
+      su[g] = 0;
+      nu[g] = 1;
+    }
+    for (bool any = true; any;) {
+      any = false;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (t[g] >= hi[g]) continue;
+        any = true;
+        const int st = ring[g] % S, u = ring[g] / S;
+        if (u > 0 && !mbar_test(bars + G * S + g * S + st, (u - 1) & 1)) continue;
+        sus_issue<Q, DMAX, MARKOV>(a, t[g], su[g], lvl_begin, ncols, stages + (size_t)(g * S + st) * Sh::STAGE_B,
+                                   bars + g * S + st, nu[g]);
+        ++ring[g];
+        if (++su[g] >= nu[g]) {
+          su[g] = 0;
+          ++t[g];
+        }
+      }
+    }
+    return;
+  }
+  const int cw = warp - 1, g = cw / T, c = cw % T;
+  unsigned char *scr = stages + (size_t)G * S * Sh::STAGE_B + (size_t)g * Sh::SCR_B;
+  double *fwd = (double *)scr;
   double *accs = fwd + Sh::FWD_D;
   double *red = accs + Sh::ACC_D;
   float *rsm = (float *)(red + Sh::RED_D);
-  const bool producer = (c == 0) && (lane == 0);
-  if (producer) {
-#pragma unroll
-    for (int s = 0; s < S; ++s) mbar_init(bars + s, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  const int M = a.c.M;
-  const long long E = a.c.E;
-  const long long ntask = (long long)(*a.nactive) * ncols;
-  const long long first = (long long)blockIdx.x * G + g, stride = (long long)gridDim.x * G;
-  SusCursor cur{0, 0};
-  if (producer) {
+  long long lo, hi;
+  group_range(ntask, (long long)blockIdx.x * G + g, ngroups, lo, hi);
+  int rr = 0;  // units consumed by this group
+  for (long long task = lo; task < hi; ++task) {
+    int nunits = 1;
 #pragma unroll 1
-    for (int n = 0; n < S; ++n)
-      sus_issue<Q, DMAX, MARKOV>(a, cur, first, stride, ntask, lvl_begin, ncols, stg + n * Sh::STAGE_F, bars + n);
-  }
-  long long u = 0;  // units consumed
-  for (long long n = 0;; ++n) {
-    const long long task = first + n * stride;
-    if (task >= ntask) break;
-    const int fb = a.list[task / ncols];
-    const int j = __ldg(a.c.level_cols + lvl_begin + (int)(task % ncols));
-    const int e0 = __ldg(a.c.col_ptr + j), dv = __ldg(a.c.col_ptr + j + 1) - e0;
-    const int nunits = dv > 0 ? dv : 1;
-    const bool frozen = lane_frozen(a, fb, lane);
-#pragma unroll 1
-    for (int s = 0; s < nunits; ++s, ++u) {
-      const int st = (int)(u % S);
-      const float *in = stg + st * Sh::STAGE_F;
+    for (int s = 0; s < nunits; ++s, ++rr) {
+      const int st = rr % S;
+      unsigned char *sb = stages + (size_t)(g * S + st) * Sh::STAGE_B;
+      uint64_t *empty = bars + G * S + g * S + st;
+      mbar_wait(bars + g * S + st, (uint32_t)((rr / S) & 1));
+      const TaskInfo ti = *(const TaskInfo *)sb;
+      const int fb = ti.fb, j = ti.item, dv = ti.deg;
+      nunits = dv > 0 ? dv : 1;
+      const bool last = (s == nunits - 1);
+      const bool frozen = a.early_exit && ((const int *)(sb + 384))[lane] != 0;
       if (dv > 0) {
-        const int e = __ldg(a.c.col_edge + e0 + s);
-        const int i = __ldg(a.c.edge_check + e);
-        const int r0 = __ldg(a.c.row_ptr + i), d = __ldg(a.c.row_ptr + i + 1) - r0;
-        const int pos = e - r0;
-        const int z = a.z[((size_t)fb * M + i) * 32 + lane];
-        mbar_wait(bars + st, (uint32_t)((u / S) & 1));
+        const SusDesc *sd = (const SusDesc *)(sb + 128);
+        const int d = ti.d;
+        const int z = sb[256 + lane];
+        const float *in = (const float *)(sb + kHdr) + lane;
+        int bbe[P];
+        unpack_basis<P>(sd->perm_e, bbe);
         double v[DO > 0 ? DO : 1][KR];
 #pragma unroll
         for (int t = 0; t < DO; ++t) {
           if (t < d - 1) {
-            const int ee = r0 + (t < pos ? t : t + 1);
             int bb[P];
-            unpack_basis<P>(__ldg(a.c.edge_perm + ee), bb);
+            unpack_basis<P>(sd->perm_o[t], bb);
             const int rch = row_hi<P, LKR>(bb, c);
 #pragma unroll
-            for (int k = 0; k < KR; ++k) v[t][k] = (double)in[(t * Q + (rch ^ row_lo<P, LKR>(bb, k))) * 32 + lane];
-            wht_bits<KR, 0, LKR>(v[t]);
+            for (int k = 0; k < KR; ++k) v[t][k] = (double)in[(t * Q + (rch ^ row_lo<P, LKR>(bb, k))) * 32];
           }
         }
+        if (!last) release_stage(empty, lane);
+#pragma unroll
+        for (int t = 0; t < DO; ++t)
+          if (t < d - 1) wht_bits<KR, 0, LKR>(v[t]);
         if constexpr (T > 1) {
 #pragma unroll
           for (int t = 0; t < DO; ++t)
@@ -827,38 +928,36 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
           for (int k = 0; k < KR; ++k) acc[k] = accs[((size_t)c * KR + k) * 32 + lane];
         }
         wht_bits<KR, 0, LKR>(acc);
-        int bb[P];
-        unpack_basis<P>(__ldg(a.c.edge_perm + e), bb);
-        const int rch = row_hi<P, LKR>(bb, c);
-        float *rdst = (a.rmsg && !frozen) ? a.rmsg + ((size_t)fb * E + e0 + s) * Q * 32 + lane : nullptr;
+        const int rch = row_hi<P, LKR>(bbe, c);
+        float *rdst = (a.rmsg && !frozen) ? a.rmsg + ((size_t)fb * E + ti.e0 + s) * Q * 32 + lane : nullptr;
 #pragma unroll
         for (int k = 0; k < KR; ++k) {
           const double x = acc[k] * (1.0 / Q);
           const float fv = (float)(x > 0.0 ? x : 0.0);
-          const int row = rch ^ row_lo<P, LKR>(bb, k);  // a = h_e^-1 y
+          const int row = rch ^ row_lo<P, LKR>(bbe, k);  // a = h_e^-1 y
           rsm[((size_t)s * Q + row) * 32 + lane] = fv;
           if (rdst) rdst[row * 32] = fv;
         }
-      } else {
-        mbar_wait(bars + st, (uint32_t)((u / S) & 1));
       }
-      if (s == nunits - 1) {
+      if (last) {
         // vertical update of column j from the fresh r's (SUS step 2)
         group_bar<T>(g);  // rsm complete
+        const VarDesc *vd = (const VarDesc *)(sb + 192);
+        int qdst[DVMAX];
         double r[DVMAX][KR];
 #pragma unroll
         for (int ss = 0; ss < DVMAX; ++ss)
-          if (ss < dv)
+          if (ss < dv) {
+            qdst[ss] = vd->qdst[ss];
 #pragma unroll
             for (int k = 0; k < KR; ++k) r[ss][k] = (double)rsm[((size_t)ss * Q + c * KR + k) * 32 + lane];
+          }
         double pr[KR];
-        prior_from<Q, KR, MARKOV>(a, j, c, lane, in + (size_t)DO * Q * 32, pr);
-        vn_body<Q, KR, DVMAX, MARKOV>(a, fb, j, e0, dv, r, pr, red, g, c, lane, frozen);
+        prior_from<Q, KR, MARKOV>(a, j, c, lane, (const float *)(sb + kHdr) + (size_t)DO * Q * 32, pr);
+        release_stage(empty, lane);
+        vn_body<Q, KR, DVMAX, MARKOV>(a, fb, j, dv, qdst, r, pr, red, g, c, lane, frozen);
       }
-      group_bar<T>(g);  // stage st (and the transpose / reduction scratch) free
-      if (producer)
-        sus_issue<Q, DMAX, MARKOV>(a, cur, first, stride, ntask, lvl_begin, ncols, stg + st * Sh::STAGE_F,
-                                   bars + st);
+      group_bar<T>(g);  // transpose / reduction scratch and rsm free
     }
   }
 }
@@ -877,9 +976,15 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
   set_error("unsupported q"); \
   return GFQ_EUNSUPPORTED;
 
-constexpr int kStagesCN = 4;
-constexpr int kStagesVN = 4;
-constexpr int kStagesSUS = 3;
+#ifndef GFQ_STAGES_CN
+#define GFQ_STAGES_CN 3
+#endif
+#ifndef GFQ_STAGES_VN
+#define GFQ_STAGES_VN 3
+#endif
+#ifndef GFQ_STAGES_SUS
+#define GFQ_STAGES_SUS 2
+#endif
 
 static int too_big(const char *what) {
   set_error(std::string(what) + ": this (q, degree) combination does not fit in shared memory");
@@ -888,9 +993,9 @@ static int too_big(const char *what) {
 
 template <int Q, int DM>
 static int cn_launch(const WaveArgs &a, cudaStream_t s) {
-  constexpr int KR = KRof<Q>::v, T = Q / KR, G = Gof<T>::v;
+  constexpr int KR = KRof<Q, KCN>::v, T = Q / KR, G = Gof<T>::v;
   using S1 = CNShape<Q, KR, DM, 1, G>;
-  constexpr int NS = fit_stages(G * S1::STAGE_F * 4, G * (128 + S1::XP_D * 8), kStagesCN);
+  constexpr int NS = fit_stages(G * S1::STAGE_B, S1::BARS_B + G * S1::SCR_B, GFQ_STAGES_CN);
   using Sh = CNShape<Q, KR, DM, NS, G>;
   if (Sh::SMEM > 232448) return too_big("k_cn");
   auto k = k_cn<Q, KR, DM, NS, G>;
@@ -906,9 +1011,9 @@ static int cn_q(const WaveArgs &a, cudaStream_t s) {
 
 template <int Q, int DV, bool MK>
 static int vn_launch(const WaveArgs &a, int clip, cudaStream_t s) {
-  constexpr int KR = KRof<Q>::v, T = Q / KR, G = Gof<T>::v;
+  constexpr int KR = KRof<Q, KVN>::v, T = Q / KR, G = Gof<T>::v;
   using S1 = VNShape<Q, KR, DV, MK, 1, G>;
-  constexpr int NS = fit_stages(G * S1::STAGE_F * 4, G * (128 + S1::RED_D * 8), kStagesVN);
+  constexpr int NS = fit_stages(G * S1::STAGE_B, S1::BARS_B + G * S1::SCR_B, GFQ_STAGES_VN);
   using Sh = VNShape<Q, KR, DV, MK, NS, G>;
   if (Sh::SMEM > 232448) return too_big("k_vn");
   auto k = k_vn<Q, KR, DV, MK, NS, G>;
@@ -919,16 +1024,16 @@ static int vn_launch(const WaveArgs &a, int clip, cudaStream_t s) {
 
 template <int Q>
 static int vn_q(const WaveArgs &a, int clip, cudaStream_t s) {
-  const bool small = a.c.max_vdeg <= 4;
-  if (a.markov) return small ? vn_launch<Q, 4, true>(a, clip, s) : vn_launch<Q, 8, true>(a, clip, s);
-  return small ? vn_launch<Q, 4, false>(a, clip, s) : vn_launch<Q, 8, false>(a, clip, s);
+  const bool small = a.c.max_vdeg <= 3;
+  if (a.markov) return small ? vn_launch<Q, 3, true>(a, clip, s) : vn_launch<Q, 8, true>(a, clip, s);
+  return small ? vn_launch<Q, 3, false>(a, clip, s) : vn_launch<Q, 8, false>(a, clip, s);
 }
 
 template <int Q, int DM, int DV, bool MK>
 static int sus_launch(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
-  constexpr int KR = KRof<Q>::v, T = Q / KR, G = Gof<T>::v;
+  constexpr int KR = KRof<Q, KSUS>::v, T = Q / KR, G = Gof<T>::v;
   using S1 = SUSShape<Q, KR, DM, DV, MK, 1, G>;
-  constexpr int NS = fit_stages(G * S1::STAGE_F * 4, S1::SMEM - G * S1::STAGE_F * 4, kStagesSUS);
+  constexpr int NS = fit_stages(G * S1::STAGE_B, S1::BARS_B + G * S1::SCR_B, GFQ_STAGES_SUS);
   using Sh = SUSShape<Q, KR, DM, DV, MK, NS, G>;
   if (Sh::SMEM > 232448) return too_big("k_sus");
   auto k = k_sus<Q, KR, DM, DV, MK, NS, G>;
@@ -939,10 +1044,10 @@ static int sus_launch(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
 
 template <int Q>
 static int sus_q(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
-  const bool small = a.c.max_cdeg <= 4 && a.c.max_vdeg <= 4;
+  const bool small = a.c.max_cdeg <= 4 && a.c.max_vdeg <= 3;
   if (a.markov)
-    return small ? sus_launch<Q, 4, 4, true>(a, lb, ncols, s) : sus_launch<Q, 8, 8, true>(a, lb, ncols, s);
-  return small ? sus_launch<Q, 4, 4, false>(a, lb, ncols, s) : sus_launch<Q, 8, 8, false>(a, lb, ncols, s);
+    return small ? sus_launch<Q, 4, 3, true>(a, lb, ncols, s) : sus_launch<Q, 8, 8, true>(a, lb, ncols, s);
+  return small ? sus_launch<Q, 4, 3, false>(a, lb, ncols, s) : sus_launch<Q, 8, 8, false>(a, lb, ncols, s);
 }
 
 int launch_cn(const WaveArgs &a, cudaStream_t s) {

@@ -165,6 +165,42 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
     for (int j = 0; j < V; ++j) level_cols[fill[lvl[j] - 1]++] = j;
   }
 
+  // static task tables (see gfq_internal.cuh)
+  std::vector<CheckDesc> cdesc(M);
+  std::vector<VarDesc> vdesc(V);
+  std::vector<SusDesc> sdesc(E);
+  memset(cdesc.data(), 0, sizeof(CheckDesc) * M);
+  memset(vdesc.data(), 0, sizeof(VarDesc) * V);
+  memset(sdesc.data(), 0, sizeof(SusDesc) * E);
+  for (int i = 0; i < M; ++i)
+    for (int s = 0; s < row_ptr[i + 1] - row_ptr[i]; ++s) {
+      cdesc[i].perm[s] = edge_perm[row_ptr[i] + s];
+      cdesc[i].canon[s] = edge_canon[row_ptr[i] + s];
+    }
+  for (int j = 0; j < V; ++j)
+    for (int s = 0; s < col_ptr[j + 1] - col_ptr[j]; ++s) vdesc[j].qdst[s] = col_edge[col_ptr[j] + s];
+  for (long long cpos = 0; cpos < E; ++cpos) {
+    const int e = col_edge[cpos], i = edge_check[e];
+    int t = 0;
+    for (int k = row_ptr[i]; k < row_ptr[i + 1]; ++k)
+      if (k != e) sdesc[cpos].perm_o[t++] = edge_perm[k];
+    sdesc[cpos].perm_e = edge_perm[e];
+  }
+  std::vector<LvlCol> lcol(V);
+  std::vector<LvlUnit> lunit;
+  lunit.reserve(E + V);
+  for (int k = 0; k < V; ++k) {
+    const int j = level_cols[k];
+    const int e0 = col_ptr[j], dv = col_ptr[j + 1] - e0;
+    lcol[k] = LvlCol{j, e0, dv, (int)lunit.size()};
+    if (dv == 0) lunit.push_back(LvlUnit{0, 0, 0, 0});
+    for (int s = 0; s < dv; ++s) {
+      const int e = col_edge[e0 + s], i = edge_check[e];
+      lunit.push_back(LvlUnit{row_ptr[i], row_ptr[i + 1] - row_ptr[i], e - row_ptr[i], i});
+    }
+  }
+  const size_t U = lunit.size();
+
   std::vector<unsigned char> mul((size_t)q * q);
   for (int x = 0; x < q; ++x)
     for (int y = 0; y < q; ++y) mul[x * q + y] = (unsigned char)gf.mul(x, y);
@@ -183,6 +219,11 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   const size_t o_lptr = off; off += al(sizeof(int) * (nlev + 1));
   const size_t o_lcol = off; off += al(sizeof(int) * V);
   const size_t o_mul = off; off += al((size_t)q * q);
+  const size_t o_cdesc = off; off += al(sizeof(CheckDesc) * M);
+  const size_t o_vdesc = off; off += al(sizeof(VarDesc) * V);
+  const size_t o_sdesc = off; off += al(sizeof(SusDesc) * E);
+  const size_t o_lvlcol = off; off += al(sizeof(LvlCol) * V);
+  const size_t o_lunit = off; off += al(sizeof(LvlUnit) * U);
   std::vector<unsigned char> host(off, 0);
   auto put = [&](size_t o, const void *src, size_t n) { if (n) memcpy(host.data() + o, src, n); };
   put(o_row, row_ptr.data(), sizeof(int) * (M + 1));
@@ -196,6 +237,11 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   put(o_lptr, level_ptr.data(), sizeof(int) * (nlev + 1));
   put(o_lcol, level_cols.data(), sizeof(int) * V);
   put(o_mul, mul.data(), (size_t)q * q);
+  put(o_cdesc, cdesc.data(), sizeof(CheckDesc) * M);
+  put(o_vdesc, vdesc.data(), sizeof(VarDesc) * V);
+  put(o_sdesc, sdesc.data(), sizeof(SusDesc) * E);
+  put(o_lvlcol, lcol.data(), sizeof(LvlCol) * V);
+  put(o_lunit, lunit.data(), sizeof(LvlUnit) * U);
 
   int dev = 0;
   cudaError_t ce = cudaGetDevice(&dev);
@@ -226,6 +272,11 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   c->d.level_ptr = (const int *)(b + o_lptr);
   c->d.level_cols = (const int *)(b + o_lcol);
   c->d.mul = b + o_mul;
+  c->d.check_desc = (const CheckDesc *)(b + o_cdesc);
+  c->d.var_desc = (const VarDesc *)(b + o_vdesc);
+  c->d.sus_desc = (const SusDesc *)(b + o_sdesc);
+  c->d.lvl_col = (const LvlCol *)(b + o_lvlcol);
+  c->d.lvl_unit = (const LvlUnit *)(b + o_lunit);
   *out = c;
   return GFQ_OK;
 }

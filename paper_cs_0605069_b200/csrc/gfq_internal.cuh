@@ -21,6 +21,29 @@ namespace gfq {
 constexpr int kLanes = 32;  // frames per block
 constexpr int kMaxDeg = 8;  // supported check / variable degree
 
+// -------------------------------------------------------------- static task tables
+// Per-task metadata that the hot kernels fetch with the Tensor Memory
+// Accelerator together with the messages (so consumer warps never wait on a
+// dependent global load).  Built once per code by gfq_code_create.
+struct __align__(128) CheckDesc {      // one per check i (PUS check node)
+  unsigned long long perm[kMaxDeg];    // packed basis images h^-1 * 2^b of edge row_ptr[i]+s
+  int canon[kMaxDeg];                  // canonical (variable-major) position of that edge
+};
+struct __align__(64) VarDesc {         // one per variable j (variable node)
+  int qdst[kMaxDeg];                   // check-major id of the edge of check slot s
+};
+struct __align__(64) SusDesc {         // one per canonical edge (j, s) (SUS unit)
+  unsigned long long perm_o[kMaxDeg - 1];  // other edges of the check, row order, skipping e
+  unsigned long long perm_e;               // the edge itself
+};
+struct __align__(16) LvlCol {          // SUS level schedule, level order
+  int j, e0, dv, unit0;                // column, its first canonical edge, degree, first unit
+};
+struct __align__(16) LvlUnit {         // one per (column, check slot) in level order
+  int r0, d, pos, i;                   // check row start / degree, position of e in the row, check
+};
+static_assert(sizeof(CheckDesc) == 128 && sizeof(VarDesc) == 64 && sizeof(SusDesc) == 64, "desc sizes");
+
 // -------------------------------------------------------------- code object
 struct DevCode {
   int p, q, N, M, V;
@@ -37,6 +60,11 @@ struct DevCode {
   const int *level_ptr;      // [L+1]   SUS dependency levels
   const int *level_cols;     // [V]
   const unsigned char *mul;  // [q*q]   GF(2^p) product table
+  const CheckDesc *check_desc;  // [M]
+  const VarDesc *var_desc;      // [V]
+  const SusDesc *sus_desc;      // [E] canonical order
+  const LvlCol *lvl_col;        // [V] level order (level_ptr delimits levels)
+  const LvlUnit *lvl_unit;      // [U] U = sum over columns of max(dv, 1)
 };
 
 }  // namespace gfq

@@ -14,7 +14,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgfq.so")
+LIB_PATH = os.environ.get("GFQ_LIB_PATH") or os.path.join(_HERE, "libgfq.so")
 
 GFQ_OK, GFQ_EINVAL, GFQ_ENOMEM, GFQ_ECUDA, GFQ_EUNSUPPORTED = 0, -1, -2, -3, -4
 GFQ_BSC, GFQ_BEC, GFQ_BIAWGN = 0, 1, 2
