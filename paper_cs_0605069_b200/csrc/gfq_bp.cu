@@ -57,10 +57,10 @@ struct QC {
 
 // entries per thread by field size and kernel (tuning knobs)
 #ifndef GFQ_KR_CN16
-#define GFQ_KR_CN16 16
+#define GFQ_KR_CN16 8
 #endif
 #ifndef GFQ_KR_VN16
-#define GFQ_KR_VN16 16
+#define GFQ_KR_VN16 8
 #endif
 #ifndef GFQ_KR_SUS16
 #define GFQ_KR_SUS16 8
@@ -174,55 +174,17 @@ __device__ __forceinline__ double neg_if(double v, int s) {
   return __longlong_as_double(__double_as_longlong(v) ^ ((long long)s << 63));
 }
 
+// Flip the sign of a double by XOR-ing its high word with a 0 / 0x80000000 mask.
+__device__ __forceinline__ double flip(double v, uint32_t m) {
+  const int lo = __double2loint(v), hi = __double2hiint(v);
+  return __hiloint2double(hi ^ (int)m, lo);
+}
+
 // Early exit freezes a converged frame: its lane keeps computing (warp-uniform
 // control flow) but stores nothing.  Invalid lanes of a ragged last block are
 // marked converged from the start.
-__device__ __forceinline__ bool lane_frozen(const WaveArgs &a, int fb, int lane) {
-  return a.early_exit && a.conv[fb * 32 + lane] != 0;
-}
 
-// Leave-one-out products in place: u[s] <- prod_{s' != s, s' < d} u[s'] (d <= DM).
-template <int DM, int KR>
-__device__ __forceinline__ void leave_one_out(double (&u)[DM][KR], int d) {
-#pragma unroll
-  for (int k = 0; k < KR; ++k) {
-    if (d == 1) {
-      u[0][k] = 1.0;
-    } else if (d == 2) {
-      const double t = u[0][k];
-      u[0][k] = u[1][k];
-      u[1][k] = t;
-    } else if (d == 3) {
-      const double a = u[0][k], b = u[1][k], c = u[2][k];
-      u[0][k] = b * c;
-      u[1][k] = a * c;
-      u[2][k] = a * b;
-    } else if (DM >= 4 && d == 4) {
-      const double ab = u[0][k] * u[1][k], cd = u[2][k] * u[3][k];
-      const double n0 = u[1][k] * cd, n1 = u[0][k] * cd;
-      const double n2 = ab * u[3][k], n3 = ab * u[2][k];
-      u[0][k] = n0; u[1][k] = n1; u[2][k] = n2; u[3][k] = n3;
-    } else if (DM > 4) {  // generic prefix/suffix for 5..8
-      double pre[DM];
-      double acc = 1.0;
-#pragma unroll
-      for (int s = 0; s < DM; ++s) {
-        pre[s] = acc;
-        if (s < d) acc *= u[s][k];
-      }
-      acc = 1.0;
-#pragma unroll
-      for (int s = DM - 1; s >= 0; --s) {
-        if (s < d) {
-          const double o = u[s][k];
-          u[s][k] = pre[s] * acc;
-          acc *= o;
-        }
-      }
-    }
-  }
-}
-
+// ============================================================== PTX: more mbarrier / shared access
 __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -238,6 +200,11 @@ __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
 }
 
 // A consumer warp is done reading a stage: one arrival per warp on its
@@ -257,17 +224,87 @@ __device__ __forceinline__ void group_range(long long ntask, long long gg, long 
 }
 
 // Stage header written by the producer (plain shared store, published by the
-// mbarrier arrive): task coordinates.
+// mbarrier arrive) followed by TMA-fetched metadata:
+//   [0,64) TaskInfo  [128,256) CheckDesc | SusDesc(128..192) + VarDesc(192..256)
+//   [256,288) syndrome row z (u8 x 32)   [384,512) frame-state row (int x 32)
 struct __align__(16) TaskInfo {
   int fb, item, e0, deg;  // block, check/variable, first edge, degree
   int s, r0, d, pos;      // SUS unit: check slot, check row start / degree, position of e
   int i, pad0, pad1, pad2;
 };
+constexpr int kHdr = 512;
+
+// Rows of one message of a thread in layout A: y = c*KR + k, k < KR.  With the
+// message slot aligned to q*128 bytes in shared memory, the byte address of
+// row (h^-1 y) is  base ^ (h^-1 y)*128  (XOR == ADD, no carries), and h^-1 y
+// = h^-1(c*KR) ^ h^-1(k): one LOP3 per entry.
+template <int P, int LKR, int KR>
+__device__ __forceinline__ void perm_addrs(uint32_t base, unsigned long long pk, int c, uint32_t (&ad)[KR],
+                                           int &rows_hi) {
+  int bb[P];
+  unpack_basis<P>(pk, bb);
+  const int rh = row_hi<P, LKR>(bb, c);
+  rows_hi = rh;
+  const uint32_t b0 = base ^ ((uint32_t)rh << 7);
+#pragma unroll
+  for (int k = 0; k < KR; ++k) ad[k] = b0 ^ ((uint32_t)row_lo<P, LKR>(bb, k) << 7);
+}
+
+// ============================================================== leave-one-out with the syndrome sign
+// out_s = sign * prod_{s' != s} u_s'   for exact degree D (sign folded in as an
+// XOR of the high word: the same sign multiplies every output at frequency w).
+template <int D, int KR, int DM>
+__device__ __forceinline__ void loo_signed(double (&u)[DM][KR], const uint32_t (&sm)[KR]) {
+#pragma unroll
+  for (int k = 0; k < KR; ++k) {
+    const uint32_t s = sm[k];
+    if constexpr (D == 1) {
+      u[0][k] = flip(1.0, s);
+    } else if constexpr (D == 2) {
+      const double t = u[0][k];
+      u[0][k] = flip(u[1][k], s);
+      u[1][k] = flip(t, s);
+    } else if constexpr (D == 3) {
+      const double a = u[0][k], b = u[1][k], cs = flip(u[2][k], s);
+      u[0][k] = b * cs;
+      u[1][k] = a * cs;
+      u[2][k] = flip(a * b, s);
+    } else if constexpr (D == 4) {
+      const double ab = flip(u[0][k] * u[1][k], s), cd = flip(u[2][k] * u[3][k], s);
+      const double n0 = u[1][k] * cd, n1 = u[0][k] * cd;
+      const double n2 = ab * u[3][k], n3 = ab * u[2][k];
+      u[0][k] = n0; u[1][k] = n1; u[2][k] = n2; u[3][k] = n3;
+    } else {
+      double pre[D];
+      double acc = 1.0;
+#pragma unroll
+      for (int t = 0; t < D; ++t) {
+        pre[t] = acc;
+        acc *= u[t][k];
+      }
+      acc = 1.0;
+#pragma unroll
+      for (int t = D - 1; t >= 0; --t) {
+        const double o = u[t][k];
+        u[t][k] = flip(pre[t] * acc, s);
+        acc *= o;
+      }
+    }
+  }
+}
+
+// Sign masks of the syndrome shift: bit 31 set where (-1)^{popc(w & z)} = -1,
+// w = k*T + c (layout B) or k (T = 1).
+template <int KR, int T>
+__device__ __forceinline__ void sign_masks(int z, int c, uint32_t (&sm)[KR]) {
+  constexpr int LT = ilog2(T);
+  const int zk = z >> LT;
+  const uint32_t base = (T > 1) ? ((uint32_t)(__popc(z & c & (T - 1)) & 1) << 31) : 0u;
+#pragma unroll
+  for (int k = 0; k < KR; ++k) sm[k] = base ^ ((uint32_t)(__popc(zk & k) & 1) << 31);
+}
 
 // ============================================================== priors
-// Extra rows a variable task needs besides its r messages, fetched into the
-// stage after them: noise symbol -> its p per-bit flip probabilities; Markov
-// source symbol (iteration >= 2) -> the posterior snapshots of j-1 and j+1.
 template <int Q, bool MARKOV>
 struct Extra {
   static constexpr int P = ilog2(Q);
@@ -283,6 +320,8 @@ __device__ __forceinline__ uint32_t extras_bytes(const WaveArgs &a, int j) {
   return 0;
 }
 
+// noise symbol -> its p per-bit flip probabilities (slot 0); Markov source
+// symbol at iteration >= 2 -> posterior snapshots of j-1 (slot 0) and j+1 (slot 1)
 template <int Q, bool MARKOV>
 __device__ __forceinline__ void issue_extras(const WaveArgs &a, int fb, int j, unsigned char *dst, uint64_t *bar) {
   constexpr int P = ilog2(Q);
@@ -295,9 +334,9 @@ __device__ __forceinline__ void issue_extras(const WaveArgs &a, int fb, int j, u
   }
 }
 
-// Prior p_j^a for the KR entries a = c*KR + k (layout A) of this thread, from
-// the extra rows in shared memory (ex):
-//  - noise symbol j = N + m: prod_b (bit_b(a) ? pi_b : 1 - pi_b)
+// Prior p_j^a for the KR entries a = c*KR + k (layout A) of this thread:
+//  - noise symbol j = N + m: prod_b (bit_b(a) ? pi_b : 1 - pi_b),
+//    built as a tensor product over the low bits;
 //  - source symbol, i.i.d. or first iteration: pi0(a)
 //  - source symbol, Markov, iteration t >= 2: Eq. (7) from the
 //    posterior snapshot Q^(t-1) of the neighbours (reading A9), boundaries A10:
@@ -315,12 +354,15 @@ __device__ __forceinline__ void prior_from(const WaveArgs &a, int j, int c, int 
     double hi = 1.0;
 #pragma unroll
     for (int b = LKR; b < P; ++b) hi *= ((c >> (b - LKR)) & 1) ? pb[b] : 1.0 - pb[b];
+    pr[0] = hi;
 #pragma unroll
-    for (int k = 0; k < KR; ++k) {
-      double v = hi;
+    for (int b = 0; b < LKR; ++b) {
+      const double one = 1.0 - pb[b];
 #pragma unroll
-      for (int b = 0; b < LKR; ++b) v *= ((k >> b) & 1) ? pb[b] : 1.0 - pb[b];
-      pr[k] = v;
+      for (int k = 0; k < (1 << b); ++k) {
+        pr[k | (1 << b)] = pr[k] * pb[b];
+        pr[k] = pr[k] * one;
+      }
     }
     return;
   }
@@ -330,8 +372,8 @@ __device__ __forceinline__ void prior_from(const WaveArgs &a, int j, int c, int 
     return;
   }
   double L[KR], R[KR];
-  const float *exl = ex;
-  const float *exr = ex + (j > 0 ? Q * 32 : 0);
+  const float *exl = ex;           // rows of j-1 (issue_extras: slot 0)
+  const float *exr = ex + Q * 32;  // rows of j+1 (slot 1)
   if (j > 0) {
 #pragma unroll
     for (int k = 0; k < KR; ++k) L[k] = 0.0;
@@ -365,148 +407,169 @@ __device__ __forceinline__ void prior_from(const WaveArgs &a, int j, int c, int 
 // ============================================================== variable node
 // Eq. (4): q_ij^a = alpha_ij p_j^a prod_{i' != i} r_i'j^a, and
 // Eq. (5): Q_j^a = alpha_j p_j^a prod_i r_ij^a, clipped to the
-// smallest a within kTieRel of the maximum (reading A17).  r[s][k] holds r of
-// check slot s at a = c*KR + k; pr the prior; qdst[s] the check-major id of
-// the edge of slot s.  Writes the dv q messages, x_hat, the Markov snapshot
-// and (keep) Q.  red: group scratch of (DVMAX+3)*T*32 doubles.
-template <int Q, int KR, int DVMAX, bool MARKOV>
-__device__ __forceinline__ void vn_body(const WaveArgs &a, int fb, int j, int dv, const int (&qdst)[DVMAX],
-                                        double (&r)[DVMAX][KR], const double (&pr)[KR], double *red,
-                                        int g, int c, int lane, bool frozen) {
+// smallest a within kTieRel of the maximum (reading A17).  Exact degree DV;
+// r[s][k] holds r of check slot s at a = c*KR + k (any positive scale: every
+// output is normalised); pr the prior; qdst[s] the check-major id of the edge
+// of slot s.  red: group scratch of (DV+2)*T*32 doubles (T > 1).
+template <int Q, int KR, int DV, bool MARKOV>
+__device__ __forceinline__ void vn_core(const WaveArgs &a, int fb, int j, const int *qdst, double (&r)[DV > 0 ? DV : 1][KR],
+                                        const double (&pr)[KR], double *red, int g, int c, int lane, bool frozen) {
   constexpr int T = Q / KR;
+  constexpr int NS = DV + 1;  // sums: DV outgoing messages + the posterior
   const long long E = a.c.E;
   double tot[KR];
+  // products (leave-one-out per exact degree), in place: r[s] <- p * prod_{s' != s} r_s'
 #pragma unroll
   for (int k = 0; k < KR; ++k) {
-    double v = pr[k];
+    if constexpr (DV == 0) {
+      tot[k] = pr[k];
+    } else if constexpr (DV == 1) {
+      tot[k] = pr[k] * r[0][k];
+      r[0][k] = pr[k];
+    } else if constexpr (DV == 2) {
+      const double q0 = pr[k] * r[1][k], q1 = pr[k] * r[0][k];
+      tot[k] = q0 * r[0][k];
+      r[0][k] = q0;
+      r[1][k] = q1;
+    } else if constexpr (DV == 3) {
+      const double x = pr[k] * r[0][k], bc = r[1][k] * r[2][k];
+      const double q0 = pr[k] * bc, q1 = x * r[2][k], q2 = x * r[1][k];
+      tot[k] = x * bc;
+      r[0][k] = q0; r[1][k] = q1; r[2][k] = q2;
+    } else {
+      double pre[DV];
+      double acc = pr[k];
 #pragma unroll
-    for (int s = 0; s < DVMAX; ++s)
-      if (s < dv) v *= r[s][k];
-    tot[k] = v;
-  }
-  if (dv > 0) leave_one_out<DVMAX, KR>(r, dv);
-  double sums[DVMAX + 1];
-#pragma unroll
-  for (int s = 0; s <= DVMAX; ++s) sums[s] = 0.0;
-  double best = 0.0;
-#pragma unroll
-  for (int k = 0; k < KR; ++k) {
-#pragma unroll
-    for (int s = 0; s < DVMAX; ++s)
-      if (s < dv) {
-        r[s][k] *= pr[k];
-        sums[s] += r[s][k];
+      for (int s = 0; s < DV; ++s) {
+        pre[s] = acc;
+        acc *= r[s][k];
       }
-    sums[DVMAX] += tot[k];
-    best = fmax(best, tot[k]);
+      tot[k] = acc;
+      acc = 1.0;
+#pragma unroll
+      for (int s = DV - 1; s >= 0; --s) {
+        const double o = r[s][k];
+        r[s][k] = pre[s] * acc;
+        acc *= o;
+      }
+    }
+  }
+  double sums[NS];
+  double mx = tot[0];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) sums[s] = 0.0;
+#pragma unroll
+  for (int k = 0; k < KR; ++k) {
+#pragma unroll
+    for (int s = 0; s < DV; ++s) sums[s] += r[s][k];
+    sums[DV] += tot[k];
+    if (k > 0) mx = fmax(mx, tot[k]);
   }
   if constexpr (T > 1) {
-    // cross-warp reduction of the sums and of the maximum
+    // two-step cross-warp reduction: partials -> warp v reduces value v -> totals
 #pragma unroll
-    for (int s = 0; s <= DVMAX; ++s)
-      if (s < dv || s == DVMAX) red[((size_t)s * T + c) * 32 + lane] = sums[s];
-    red[((size_t)(DVMAX + 1) * T + c) * 32 + lane] = best;
+    for (int s = 0; s < NS; ++s) red[((size_t)s * T + c) * 32 + lane] = sums[s];
+    red[((size_t)NS * T + c) * 32 + lane] = mx;
+    group_bar<T>(g);
+    double *tot_s = red + (size_t)(NS + 1) * T * 32;
+#pragma unroll 1
+    for (int vi = c; vi <= NS; vi += T) {
+      double v = red[((size_t)vi * T) * 32 + lane];
+#pragma unroll
+      for (int cc = 1; cc < T; ++cc) {
+        const double w = red[((size_t)vi * T + cc) * 32 + lane];
+        v = (vi == NS) ? fmax(v, w) : v + w;
+      }
+      tot_s[vi * 32 + lane] = v;
+    }
     group_bar<T>(g);
 #pragma unroll
-    for (int s = 0; s <= DVMAX; ++s)
-      if (s < dv || s == DVMAX) {
-        double t = 0.0;
-#pragma unroll
-        for (int cc = 0; cc < T; ++cc) t += red[((size_t)s * T + cc) * 32 + lane];
-        sums[s] = t;
-      }
-#pragma unroll
-    for (int cc = 0; cc < T; ++cc) best = fmax(best, red[((size_t)(DVMAX + 1) * T + cc) * 32 + lane]);
+    for (int s = 0; s < NS; ++s) sums[s] = tot_s[s * 32 + lane];
+    mx = tot_s[NS * 32 + lane];
   }
   // Clipping: the smallest a whose Q is within kTieRel of the maximum.
-  const double thr = best * (1.0 - kTieRel);
+  const double thr = mx * (1.0 - kTieRel);
   int bidx = Q;
 #pragma unroll
   for (int k = KR - 1; k >= 0; --k)
     if (tot[k] >= thr) bidx = c * KR + k;
   if constexpr (T > 1) {
-    int *ired = (int *)(red + (size_t)(DVMAX + 2) * T * 32);
+    int *ired = (int *)(red + (size_t)(NS + 1) * T * 32 + (size_t)(NS + 1) * 32);
     ired[c * 32 + lane] = bidx;
     group_bar<T>(g);
 #pragma unroll
     for (int cc = 0; cc < T; ++cc) bidx = min(bidx, ired[cc * 32 + lane]);
   }
   if (bidx >= Q) bidx = 0;
-  if (frozen) return;  // a converged frame keeps the state it converged with
   int bad = 0;
 #pragma unroll
-  for (int s = 0; s < DVMAX; ++s) {
-    if (s < dv) {
-      float *dst = a.qmsg + ((size_t)fb * E + qdst[s]) * Q * 32 + lane;
-      const double sm = sums[s];
-      const bool ok = sm > 0.0 && isfinite(sm);
-      bad += !ok;
-      const double inv = ok ? 1.0 / sm : 0.0;
+  for (int s = 0; s < DV; ++s) {
+    const double sm = sums[s];
+    const bool ok = sm > 0.0 && isfinite(sm);
+    bad += !ok;
+    const double inv = ok ? 1.0 / sm : 0.0;
+    const float add = ok ? 0.0f : 1.0f / Q;
+    if (!frozen) {
+      float *dst = a.qmsg + ((size_t)fb * E + qdst[s]) * Q * 32 + lane + c * KR * 32;
 #pragma unroll
-      for (int k = 0; k < KR; ++k) dst[(c * KR + k) * 32] = ok ? (float)(r[s][k] * inv) : 1.0f / Q;
+      for (int k = 0; k < KR; ++k) dst[k * 32] = (float)(r[s][k] * inv) + add;
     }
   }
-  const double st = sums[DVMAX];
+  const double st = sums[DV];
   const bool okq = st > 0.0 && isfinite(st);
   bad += !okq;
   if (!okq) bidx = 0;
   const double invq = okq ? 1.0 / st : 0.0;
-  if (MARKOV && j < a.c.N && a.qs_new) {
-    float *dst = a.qs_new + ((size_t)fb * a.c.N + j) * Q * 32 + lane;
+  const float addq = okq ? 0.0f : 1.0f / Q;
+  if (!frozen) {
+    if (MARKOV && j < a.c.N && a.qs_new) {
+      float *dst = a.qs_new + ((size_t)fb * a.c.N + j) * Q * 32 + lane + c * KR * 32;
 #pragma unroll
-    for (int k = 0; k < KR; ++k) dst[(c * KR + k) * 32] = okq ? (float)(tot[k] * invq) : 1.0f / Q;
-  }
-  if (a.qall) {
-    float *dst = a.qall + ((size_t)fb * a.c.V + j) * Q * 32 + lane;
+      for (int k = 0; k < KR; ++k) dst[k * 32] = (float)(tot[k] * invq) + addq;
+    }
+    if (a.qall) {
+      float *dst = a.qall + ((size_t)fb * a.c.V + j) * Q * 32 + lane + c * KR * 32;
 #pragma unroll
-    for (int k = 0; k < KR; ++k) dst[(c * KR + k) * 32] = okq ? (float)(tot[k] * invq) : 1.0f / Q;
+      for (int k = 0; k < KR; ++k) dst[k * 32] = (float)(tot[k] * invq) + addq;
+    }
+    if (c == 0) a.xhat[((size_t)fb * a.c.V + j) * 32 + lane] = (unsigned char)bidx;
+    if (bad && c == 0) atomicAdd(a.stats + 0, (unsigned long long)bad);
   }
-  if (c == 0) a.xhat[((size_t)fb * a.c.V + j) * 32 + lane] = (unsigned char)bidx;
-  if (bad && c == 0) atomicAdd(a.stats + 0, (unsigned long long)bad);
 }
 
-// ============================================================== pipeline shapes
-// CTA = 1 producer warp (lane 0 issues every TMA copy) + G groups of T
-// consumer warps.  Group g owns a ring of S stages with "full" (TMA bytes
-// landed) and "empty" (all T warps done reading) mbarriers.
-//   stage = [TaskInfo 64B][static desc 64..128B][z 32B -> 128][conv 128B][payload]
-constexpr int kHdr = 512;  // stage header bytes (payload offset)
-
-template <int Q, int KR, int DMAX, int S, int G>
-struct CNShape {
-  static constexpr int T = Q / KR;
-  static constexpr size_t STAGE_B = kHdr + (size_t)DMAX * Q * 128;
-  static constexpr size_t SCR_B = T > 1 ? (size_t)DMAX * Q * 32 * 8 : 0;
+// ============================================================== shared-memory layout
+// [mbarriers][G*S headers of kHdr][pad][G*S payload slots, each a multiple of
+// PAL = q*128 bytes and PAL-aligned in the shared window][G scratch areas]
+template <int Q, int S, int G, size_t PAY, size_t SCR>
+struct Shape {
+  static constexpr size_t PAL = (size_t)Q * 128;
+  static constexpr size_t PAYA = ((PAY + PAL - 1) / PAL) * PAL;
   static constexpr size_t BARS_B = ((16 * S * G + 127) / 128) * 128;
-  static constexpr size_t SMEM = BARS_B + (size_t)G * S * STAGE_B + (size_t)G * SCR_B;
-  static constexpr int THREADS = (1 + G * T) * 32;
+  static constexpr size_t HDR_B = (size_t)G * S * kHdr;
+  static constexpr size_t SMEM = BARS_B + HDR_B + PAL + (size_t)G * S * PAYA + (size_t)G * SCR;
 };
 
-template <int Q, int KR, int DVMAX, bool MARKOV, int S, int G>
-struct VNShape {
-  static constexpr int T = Q / KR;
-  static constexpr int XR = Extra<Q, MARKOV>::rows;
-  static constexpr size_t STAGE_B = kHdr + ((size_t)DVMAX * Q + XR) * 128;
-  static constexpr size_t SCR_B = (size_t)(DVMAX + 3) * T * 32 * 8;
-  static constexpr size_t BARS_B = ((16 * S * G + 127) / 128) * 128;
-  static constexpr size_t SMEM = BARS_B + (size_t)G * S * STAGE_B + (size_t)G * SCR_B;
-  static constexpr int THREADS = (1 + G * T) * 32;
+struct SmemPtrs {
+  uint64_t *bars;
+  unsigned char *hdr;
+  unsigned char *pay;
+  uint32_t pay_u32;
+  unsigned char *scr;
 };
 
-template <int Q, int KR, int DMAX, int DVMAX, bool MARKOV, int S, int G>
-struct SUSShape {
-  static constexpr int T = Q / KR;
-  static constexpr int XR = Extra<Q, MARKOV>::rows;
-  static constexpr size_t STAGE_B = kHdr + ((size_t)(DMAX - 1) * Q + XR) * 128;
-  static constexpr size_t FWD_D = T > 1 ? (size_t)(DMAX - 1) * Q * 32 : 0;
-  static constexpr size_t ACC_D = T > 1 ? (size_t)Q * 32 : 0;
-  static constexpr size_t RED_D = (size_t)(DVMAX + 3) * T * 32;
-  static constexpr size_t RSM_F = (size_t)DVMAX * Q * 32;
-  static constexpr size_t SCR_B = (FWD_D + ACC_D + RED_D) * 8 + RSM_F * 4;
-  static constexpr size_t BARS_B = ((16 * S * G + 127) / 128) * 128;
-  static constexpr size_t SMEM = BARS_B + (size_t)G * S * STAGE_B + (size_t)G * SCR_B;
-  static constexpr int THREADS = (1 + G * T) * 32;
-};
+template <typename Sh, int S, int G>
+__device__ __forceinline__ SmemPtrs smem_ptrs(unsigned char *smem) {
+  SmemPtrs p;
+  p.bars = (uint64_t *)smem;
+  p.hdr = smem + Sh::BARS_B;
+  const uint32_t base = smem_u32(smem);
+  const uint32_t want = base + (uint32_t)(Sh::BARS_B + Sh::HDR_B);
+  const uint32_t al = (uint32_t)(((want + Sh::PAL - 1) / Sh::PAL) * Sh::PAL);
+  p.pay = smem + (al - base);
+  p.pay_u32 = al;
+  p.scr = p.pay + (size_t)G * S * Sh::PAYA;
+  return p;
+}
 
 template <int S, int G>
 __device__ __forceinline__ void init_bars(uint64_t *bars, int T) {
@@ -518,262 +581,329 @@ __device__ __forceinline__ void init_bars(uint64_t *bars, int T) {
   fence_mbar_init();
 }
 
+// Producer: lane 0 of warp 0 walks every consumer group's contiguous share of
+// tasks round-robin, refilling a stage as soon as its "empty" barrier flips.
+template <int S, int G, typename Issue>
+__device__ __forceinline__ void produce(uint64_t *bars, long long ntask, Issue issue) {
+  const long long ngroups = (long long)gridDim.x * G;
+  long long t[G], hi[G];
+  int ring[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    group_range(ntask, (long long)blockIdx.x * G + g, ngroups, t[g], hi[g]);
+    ring[g] = 0;
+  }
+  for (bool any = true; any;) {
+    any = false;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      if (t[g] >= hi[g]) continue;
+      any = true;
+      const int st = ring[g] % S, u = ring[g] / S;
+      if (u > 0 && !mbar_test(bars + G * S + g * S + st, (u - 1) & 1)) continue;
+      if (issue(g, st, t[g])) ++t[g];
+      ++ring[g];
+    }
+  }
+}
+
 // ============================================================== PUS: check node
+template <int Q, int KR, int DMAX, int S, int G>
+struct CNShape {
+  static constexpr int T = Q / KR;
+  static constexpr size_t PAY = (size_t)DMAX * Q * 128;
+  static constexpr size_t SCR = T > 1 ? (size_t)DMAX * Q * 32 * 8 : 0;
+  using Sh = Shape<Q, S, G, PAY, SCR>;
+  static constexpr size_t SMEM = Sh::SMEM;
+  static constexpr int THREADS = (1 + G * T) * 32;
+};
+
 template <int Q, int DMAX>
-__device__ __forceinline__ void cn_issue(const WaveArgs &a, long long task, unsigned char *sb, uint64_t *full) {
+__device__ __forceinline__ void cn_issue(const WaveArgs &a, long long task, unsigned char *hdr, unsigned char *pay,
+                                         uint64_t *full) {
   const int M = a.c.M;
   const int fb = a.list[task / M];
   const int i = (int)(task % M);
   const int e0 = __ldg(a.c.row_ptr + i), d = __ldg(a.c.row_ptr + i + 1) - e0;
-  TaskInfo *ti = (TaskInfo *)sb;
+  TaskInfo *ti = (TaskInfo *)hdr;
   ti->fb = fb; ti->item = i; ti->e0 = e0; ti->deg = d;
   const uint32_t msg = (uint32_t)d * Q * 128;
   mbar_expect_tx(full, 128 + 32 + (a.early_exit ? 128 : 0) + msg);
-  bulk_g2s(sb + 128, a.c.check_desc + i, 128, full);
-  bulk_g2s(sb + 256, a.z + ((size_t)fb * M + i) * 32, 32, full);
-  if (a.early_exit) bulk_g2s(sb + 384, a.conv + fb * 32, 128, full);
-  if (msg) bulk_g2s(sb + kHdr, a.qmsg + ((size_t)fb * a.c.E + e0) * Q * 32, msg, full);
+  bulk_g2s(hdr + 128, a.c.check_desc + i, 128, full);
+  bulk_g2s(hdr + 256, a.z + ((size_t)fb * M + i) * 32, 32, full);
+  if (a.early_exit) bulk_g2s(hdr + 384, a.conv + fb * 32, 128, full);
+  if (msg) bulk_g2s(pay, a.qmsg + ((size_t)fb * a.c.E + e0) * Q * 32, msg, full);
 }
 
-// Eq. (3) for every edge of check i (horizontal pass),
-// in the transform domain (BASELINE.json north_star): with u_k(y) =
-// q_ij_k(h_k^-1 y) (the distribution of h_k x_k), U_k = WHT(u_k),
-//   r_ij_k(a) = (1/q) WHT[ (-1)^{w.z_i} prod_{k' != k} U_k'(w) ](h_k a).
+// Eq. (3) for every edge of a check of exact degree D (horizontal
+// pass), in the transform domain (BASELINE.json north_star): with
+// u_k(y) = q_ij_k(h_k^-1 y) (the distribution of h_k x_k), U_k = WHT(u_k),
+//   r_ij_k(a) ∝ WHT[ (-1)^{w.z_i} prod_{k' != k} U_k'(w) ](h_k a).
 // The syndrome enters as the sign (-1)^{popc(w & z_i)} (XOR shift by z_i,
-// reading A4).  Negative round-off is clamped to 0 (reading A20).
-template <int Q, int KR, int DMAX, int S, int G>
-__global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(WaveArgs a) {
-  using Sh = CNShape<Q, KR, DMAX, S, G>;
+// reading A4).  The stored r is q * r (the 1/q of the inverse transform is
+// dropped: the variable node normalises, the export divides); negative
+// round-off is clamped to 0 (reading A20).
+template <int Q, int KR, int D, int DMAX>
+__device__ __forceinline__ void cn_task(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_u32,
+                                        uint64_t *empty, double *xp, int g, int c, int lane) {
   using C = QC<Q, KR>;
   constexpr int T = C::T, LKR = C::LKR, LT = C::LT, P = C::P;
+  const TaskInfo ti = *(const TaskInfo *)hdr;
+  const CheckDesc *cd = (const CheckDesc *)(hdr + 128);
+  const int fb = ti.fb;
+  const int z = hdr[256 + lane];
+  const bool frozen = a.early_exit && ((const int *)(hdr + 384))[lane] != 0;
+  const long long E = a.c.E;
+  uint32_t ad[D][KR];
+  int rh[D];
+  double u[D][KR];
+#pragma unroll
+  for (int s = 0; s < D; ++s) {
+    perm_addrs<P, LKR, KR>(pay_u32 + (uint32_t)(s * Q * 128 + lane * 4), cd->perm[s], c, ad[s], rh[s]);
+#pragma unroll
+    for (int k = 0; k < KR; ++k) u[s][k] = (double)lds_f32(ad[s][k]);
+  }
+  int canon[D];
+#pragma unroll
+  for (int s = 0; s < D; ++s) canon[s] = cd->canon[s];
+  release_stage(empty, lane);
+#pragma unroll
+  for (int s = 0; s < D; ++s) wht_bits<KR, 0, LKR>(u[s]);
+  if constexpr (T > 1) {
+#pragma unroll
+    for (int s = 0; s < D; ++s)
+#pragma unroll
+      for (int k = 0; k < KR; ++k) xp[((size_t)s * Q + c * KR + k) * 32 + lane] = u[s][k];
+    group_bar<T>(g);
+#pragma unroll
+    for (int s = 0; s < D; ++s) {
+#pragma unroll
+      for (int k = 0; k < KR; ++k) u[s][k] = xp[((size_t)s * Q + k * T + c) * 32 + lane];
+      wht_bits<KR, LKR - LT, LKR>(u[s]);
+    }
+  }
+  uint32_t sm[KR];
+  sign_masks<KR, T>(z, c, sm);
+  loo_signed<D, KR, D>(u, sm);
+  if constexpr (T > 1) {
+#pragma unroll
+    for (int s = 0; s < D; ++s) wht_bits<KR, LKR - LT, LKR>(u[s]);
+    group_bar<T>(g);
+#pragma unroll
+    for (int s = 0; s < D; ++s)
+#pragma unroll
+      for (int k = 0; k < KR; ++k) xp[((size_t)s * Q + k * T + c) * 32 + lane] = u[s][k];
+    group_bar<T>(g);
+#pragma unroll
+    for (int s = 0; s < D; ++s)
+#pragma unroll
+      for (int k = 0; k < KR; ++k) u[s][k] = xp[((size_t)s * Q + c * KR + k) * 32 + lane];
+    group_bar<T>(g);
+  }
+#pragma unroll
+  for (int s = 0; s < D; ++s) {
+    wht_bits<KR, 0, LKR>(u[s]);
+    if (!frozen) {
+      unsigned char *dst = (unsigned char *)(a.rmsg + ((size_t)fb * E + canon[s]) * Q * 32 + lane);
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        // same rows as the load: r_k(a) lands at a = h^-1 y
+        const uint32_t roff = (ad[s][k] ^ (pay_u32 + (uint32_t)(s * Q * 128 + lane * 4)));
+        *(float *)(dst + roff) = fmaxf((float)u[s][k], 0.0f);
+      }
+    }
+  }
+  (void)rh;
+}
+
+template <int Q, int KR, int DMAX, int S, int G>
+__global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(WaveArgs a) {
+  using CS = CNShape<Q, KR, DMAX, S, G>;
+  using Sh = typename CS::Sh;
+  constexpr int T = CS::T;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t *bars = (uint64_t *)smem;
-  unsigned char *stages = smem + Sh::BARS_B;
+  const SmemPtrs sp = smem_ptrs<Sh, S, G>(smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) init_bars<S, G>(bars, T);
+  if (threadIdx.x == 0) init_bars<S, G>(sp.bars, T);
   __syncthreads();
   const int M = a.c.M;
-  const long long E = a.c.E;
   const long long ntask = (long long)(*a.nactive) * M;
-  const long long ngroups = (long long)gridDim.x * G;
-  if (warp == 0) {  // ---------------- producer
-    if (lane != 0) return;
-    long long t[G], hi[G];
-    int ring[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      group_range(ntask, (long long)blockIdx.x * G + g, ngroups, t[g], hi[g]);
-      ring[g] = 0;
-    }
-    for (bool any = true; any;) {
-      any = false;
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        if (t[g] >= hi[g]) continue;
-        any = true;
-        const int st = ring[g] % S, u = ring[g] / S;
-        if (u > 0 && !mbar_test(bars + G * S + g * S + st, (u - 1) & 1)) continue;
-        cn_issue<Q, DMAX>(a, t[g], stages + (size_t)(g * S + st) * Sh::STAGE_B, bars + g * S + st);
-        ++t[g];
-        ++ring[g];
-      }
-    }
+  if (warp == 0) {
+    if (lane == 0)
+      produce<S, G>(sp.bars, ntask, [&](int g, int st, long long task) {
+        const int k = g * S + st;
+        cn_issue<Q, DMAX>(a, task, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA, sp.bars + k);
+        return true;
+      });
     return;
   }
-  // ---------------- consumers
   const int cw = warp - 1, g = cw / T, c = cw % T;
-  double *xp = (double *)(stages + (size_t)G * S * Sh::STAGE_B + (size_t)g * Sh::SCR_B);
+  double *xp = (double *)(sp.scr + (size_t)g * CS::SCR);
   long long lo, hi;
-  group_range(ntask, (long long)blockIdx.x * G + g, ngroups, lo, hi);
+  group_range(ntask, (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
   for (long long task = lo; task < hi; ++task) {
-    const int rr = (int)(task - lo), st = rr % S;
-    unsigned char *sb = stages + (size_t)(g * S + st) * Sh::STAGE_B;
-    mbar_wait(bars + g * S + st, (uint32_t)((rr / S) & 1));
-    const TaskInfo ti = *(const TaskInfo *)sb;
-    const CheckDesc *cd = (const CheckDesc *)(sb + 128);
-    const int fb = ti.fb, d = ti.deg;
-    const int z = sb[256 + lane];
-    const bool frozen = a.early_exit && ((const int *)(sb + 384))[lane] != 0;
-    const float *in = (const float *)(sb + kHdr) + lane;
-    int bb[DMAX][P];
-    int rc[DMAX];
-    int canon[DMAX];
-    double u[DMAX][KR];
-#pragma unroll
-    for (int s = 0; s < DMAX; ++s) {
-      if (s < d) {
-        unpack_basis<P>(cd->perm[s], bb[s]);
-        canon[s] = cd->canon[s];
-        rc[s] = row_hi<P, LKR>(bb[s], c);
-#pragma unroll
-        for (int k = 0; k < KR; ++k) u[s][k] = (double)in[(s * Q + (rc[s] ^ row_lo<P, LKR>(bb[s], k))) * 32];
-      }
-    }
-    release_stage(bars + G * S + g * S + st, lane);
-#pragma unroll
-    for (int s = 0; s < DMAX; ++s)
-      if (s < d) wht_bits<KR, 0, LKR>(u[s]);
-    if constexpr (T > 1) {
-#pragma unroll
-      for (int s = 0; s < DMAX; ++s)
-        if (s < d)
-#pragma unroll
-          for (int k = 0; k < KR; ++k) xp[((size_t)s * Q + c * KR + k) * 32 + lane] = u[s][k];
-      group_bar<T>(g);
-#pragma unroll
-      for (int s = 0; s < DMAX; ++s)
-        if (s < d) {
-#pragma unroll
-          for (int k = 0; k < KR; ++k) u[s][k] = xp[((size_t)s * Q + k * T + c) * 32 + lane];
-          wht_bits<KR, LKR - LT, LKR>(u[s]);
-        }
-    }
-    leave_one_out<DMAX, KR>(u, d);
-#pragma unroll
-    for (int k = 0; k < KR; ++k) {
-      const int w = (T > 1) ? (k * T + c) : k;
-      const int sg = __popc(w & z) & 1;
-#pragma unroll
-      for (int s = 0; s < DMAX; ++s)
-        if (s < d) u[s][k] = neg_if(u[s][k], sg);
-    }
-    if constexpr (T > 1) {
-#pragma unroll
-      for (int s = 0; s < DMAX; ++s)
-        if (s < d) wht_bits<KR, LKR - LT, LKR>(u[s]);
-      group_bar<T>(g);
-#pragma unroll
-      for (int s = 0; s < DMAX; ++s)
-        if (s < d)
-#pragma unroll
-          for (int k = 0; k < KR; ++k) xp[((size_t)s * Q + k * T + c) * 32 + lane] = u[s][k];
-      group_bar<T>(g);
-#pragma unroll
-      for (int s = 0; s < DMAX; ++s)
-        if (s < d)
-#pragma unroll
-          for (int k = 0; k < KR; ++k) u[s][k] = xp[((size_t)s * Q + c * KR + k) * 32 + lane];
-      group_bar<T>(g);
-    }
-    constexpr double invq = 1.0 / Q;
-#pragma unroll
-    for (int s = 0; s < DMAX; ++s) {
-      if (s < d) {
-        wht_bits<KR, 0, LKR>(u[s]);
-        if (!frozen) {
-          float *dst = a.rmsg + ((size_t)fb * E + canon[s]) * Q * 32 + lane;
-#pragma unroll
-          for (int k = 0; k < KR; ++k) {
-            const double v = u[s][k] * invq;
-            dst[(rc[s] ^ row_lo<P, LKR>(bb[s], k)) * 32] = (float)(v > 0.0 ? v : 0.0);
+    const int rr = (int)(task - lo), st = rr % S, k = g * S + st;
+    const unsigned char *hdr = sp.hdr + (size_t)k * kHdr;
+    const uint32_t pay = sp.pay_u32 + (uint32_t)((size_t)k * Sh::PAYA);
+    uint64_t *empty = sp.bars + G * S + k;
+    mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
+    const int d = ((const TaskInfo *)hdr)->deg;
+    switch (d) {
+      case 1: cn_task<Q, KR, 1, DMAX>(a, hdr, pay, empty, xp, g, c, lane); break;
+      case 2: cn_task<Q, KR, 2, DMAX>(a, hdr, pay, empty, xp, g, c, lane); break;
+      case 3: cn_task<Q, KR, 3, DMAX>(a, hdr, pay, empty, xp, g, c, lane); break;
+      case 4: cn_task<Q, KR, 4, DMAX>(a, hdr, pay, empty, xp, g, c, lane); break;
+      default:
+        if constexpr (DMAX > 4) {
+          switch (d) {
+            case 5: cn_task<Q, KR, 5, DMAX>(a, hdr, pay, empty, xp, g, c, lane); break;
+            case 6: cn_task<Q, KR, 6, DMAX>(a, hdr, pay, empty, xp, g, c, lane); break;
+            case 7: cn_task<Q, KR, 7, DMAX>(a, hdr, pay, empty, xp, g, c, lane); break;
+            default: cn_task<Q, KR, 8, DMAX>(a, hdr, pay, empty, xp, g, c, lane); break;
           }
+        } else {
+          release_stage(empty, lane);  // d == 0: an empty check has no edge
         }
-      }
+        break;
     }
   }
 }
 
 // ============================================================== PUS: variable node
+template <int Q, int KR, int DVMAX, bool MARKOV, int S, int G>
+struct VNShape {
+  static constexpr int T = Q / KR;
+  static constexpr int XR = Extra<Q, MARKOV>::rows;
+  static constexpr size_t PAY = ((size_t)DVMAX * Q + XR) * 128;
+  static constexpr size_t SCR = ((size_t)(DVMAX + 2) * T * 32 + (size_t)(DVMAX + 2) * 32 + T * 32) * 8;
+  using Sh = Shape<Q, S, G, PAY, SCR>;
+  static constexpr size_t SMEM = Sh::SMEM;
+  static constexpr int THREADS = (1 + G * T) * 32;
+};
+
 template <int Q, int DVMAX, bool MARKOV>
-__device__ __forceinline__ void vn_issue(const WaveArgs &a, long long task, unsigned char *sb, uint64_t *full,
-                                         int clip_only) {
+__device__ __forceinline__ void vn_issue(const WaveArgs &a, long long task, unsigned char *hdr, unsigned char *pay,
+                                         uint64_t *full, int clip_only) {
   const int V = a.c.V;
   const int fb = a.list[task / V];
   const int j = (int)(task % V);
   const int e0 = __ldg(a.c.col_ptr + j);
   const int dv = clip_only ? 0 : __ldg(a.c.col_ptr + j + 1) - e0;
-  TaskInfo *ti = (TaskInfo *)sb;
+  TaskInfo *ti = (TaskInfo *)hdr;
   ti->fb = fb; ti->item = j; ti->e0 = e0; ti->deg = dv;
   const uint32_t br = (uint32_t)dv * Q * 128;
   mbar_expect_tx(full, 64 + (a.early_exit ? 128 : 0) + br + extras_bytes<Q, MARKOV>(a, j));
-  bulk_g2s(sb + 128, a.c.var_desc + j, 64, full);
-  if (a.early_exit) bulk_g2s(sb + 384, a.conv + fb * 32, 128, full);
-  if (br) bulk_g2s(sb + kHdr, a.rmsg + ((size_t)fb * a.c.E + e0) * Q * 32, br, full);  // canonical order
-  issue_extras<Q, MARKOV>(a, fb, j, sb + kHdr + (size_t)DVMAX * Q * 128, full);
+  bulk_g2s(hdr + 192, a.c.var_desc + j, 64, full);
+  if (a.early_exit) bulk_g2s(hdr + 384, a.conv + fb * 32, 128, full);
+  if (br) bulk_g2s(pay, a.rmsg + ((size_t)fb * a.c.E + e0) * Q * 32, br, full);  // canonical order
+  issue_extras<Q, MARKOV>(a, fb, j, pay + (size_t)DVMAX * Q * 128, full);
+}
+
+template <int Q, int KR, int DV, int DVMAX, bool MARKOV>
+__device__ __forceinline__ void vn_task(const WaveArgs &a, const unsigned char *hdr, const unsigned char *pay,
+                                        uint64_t *empty, double *red, int g, int c, int lane) {
+  const TaskInfo ti = *(const TaskInfo *)hdr;
+  const VarDesc *vd = (const VarDesc *)(hdr + 192);
+  const bool frozen = a.early_exit && ((const int *)(hdr + 384))[lane] != 0;
+  const float *in = (const float *)pay + lane + c * KR * 32;
+  int qdst[DV > 0 ? DV : 1];
+  double r[DV > 0 ? DV : 1][KR];
+#pragma unroll
+  for (int s = 0; s < DV; ++s) {
+    qdst[s] = vd->qdst[s];
+#pragma unroll
+    for (int k = 0; k < KR; ++k) r[s][k] = (double)in[(s * Q + k) * 32];
+  }
+  double pr[KR];
+  prior_from<Q, KR, MARKOV>(a, ti.item, c, lane, (const float *)pay + (size_t)DVMAX * Q * 32, pr);
+  release_stage(empty, lane);
+  vn_core<Q, KR, DV, MARKOV>(a, ti.fb, ti.item, qdst, r, pr, red, g, c, lane, frozen);
 }
 
 template <int Q, int KR, int DVMAX, bool MARKOV, int S, int G>
 __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
     k_vn(WaveArgs a, int clip_only) {
-  using Sh = VNShape<Q, KR, DVMAX, MARKOV, S, G>;
-  constexpr int T = Sh::T;
+  using VS = VNShape<Q, KR, DVMAX, MARKOV, S, G>;
+  using Sh = typename VS::Sh;
+  constexpr int T = VS::T;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t *bars = (uint64_t *)smem;
-  unsigned char *stages = smem + Sh::BARS_B;
+  const SmemPtrs sp = smem_ptrs<Sh, S, G>(smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) init_bars<S, G>(bars, T);
+  if (threadIdx.x == 0) init_bars<S, G>(sp.bars, T);
   __syncthreads();
   const int V = a.c.V;
   const long long ntask = (long long)(*a.nactive) * V;
-  const long long ngroups = (long long)gridDim.x * G;
-  if (warp == 0) {  // ---------------- producer
-    if (lane != 0) return;
-    long long t[G], hi[G];
-    int ring[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      group_range(ntask, (long long)blockIdx.x * G + g, ngroups, t[g], hi[g]);
-      ring[g] = 0;
-    }
-    for (bool any = true; any;) {
-      any = false;
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        if (t[g] >= hi[g]) continue;
-        any = true;
-        const int st = ring[g] % S, u = ring[g] / S;
-        if (u > 0 && !mbar_test(bars + G * S + g * S + st, (u - 1) & 1)) continue;
-        vn_issue<Q, DVMAX, MARKOV>(a, t[g], stages + (size_t)(g * S + st) * Sh::STAGE_B, bars + g * S + st,
+  if (warp == 0) {
+    if (lane == 0)
+      produce<S, G>(sp.bars, ntask, [&](int g, int st, long long task) {
+        const int k = g * S + st;
+        vn_issue<Q, DVMAX, MARKOV>(a, task, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA, sp.bars + k,
                                    clip_only);
-        ++t[g];
-        ++ring[g];
-      }
-    }
+        return true;
+      });
     return;
   }
   const int cw = warp - 1, g = cw / T, c = cw % T;
-  double *red = (double *)(stages + (size_t)G * S * Sh::STAGE_B + (size_t)g * Sh::SCR_B);
+  double *red = (double *)(sp.scr + (size_t)g * VS::SCR);
   long long lo, hi;
-  group_range(ntask, (long long)blockIdx.x * G + g, ngroups, lo, hi);
+  group_range(ntask, (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
   for (long long task = lo; task < hi; ++task) {
-    const int rr = (int)(task - lo), st = rr % S;
-    unsigned char *sb = stages + (size_t)(g * S + st) * Sh::STAGE_B;
-    mbar_wait(bars + g * S + st, (uint32_t)((rr / S) & 1));
-    const TaskInfo ti = *(const TaskInfo *)sb;
-    const VarDesc *vd = (const VarDesc *)(sb + 128);
-    const int fb = ti.fb, j = ti.item, dv = ti.deg;
-    const bool frozen = a.early_exit && ((const int *)(sb + 384))[lane] != 0;
-    const float *in = (const float *)(sb + kHdr);
-    int qdst[DVMAX];
-    double r[DVMAX][KR];
-#pragma unroll
-    for (int s = 0; s < DVMAX; ++s)
-      if (s < dv) {
-        qdst[s] = vd->qdst[s];
-#pragma unroll
-        for (int k = 0; k < KR; ++k) r[s][k] = (double)in[(s * Q + c * KR + k) * 32 + lane];
-      }
-    double pr[KR];
-    prior_from<Q, KR, MARKOV>(a, j, c, lane, in + (size_t)DVMAX * Q * 32, pr);
-    release_stage(bars + G * S + g * S + st, lane);
-    vn_body<Q, KR, DVMAX, MARKOV>(a, fb, j, dv, qdst, r, pr, red, g, c, lane, frozen);
+    const int rr = (int)(task - lo), st = rr % S, k = g * S + st;
+    const unsigned char *hdr = sp.hdr + (size_t)k * kHdr;
+    const unsigned char *pay = sp.pay + (size_t)k * Sh::PAYA;
+    uint64_t *empty = sp.bars + G * S + k;
+    mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
+    const int dv = ((const TaskInfo *)hdr)->deg;
+    switch (dv) {
+      case 0: vn_task<Q, KR, 0, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
+      case 1: vn_task<Q, KR, 1, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
+      case 2: vn_task<Q, KR, 2, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
+      default:
+        if constexpr (DVMAX <= 3) {
+          vn_task<Q, KR, 3, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane);
+        } else {
+          switch (dv) {
+            case 3: vn_task<Q, KR, 3, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
+            case 4: vn_task<Q, KR, 4, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
+            case 5: vn_task<Q, KR, 5, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
+            case 6: vn_task<Q, KR, 6, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
+            case 7: vn_task<Q, KR, 7, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
+            default: vn_task<Q, KR, 8, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
+          }
+        }
+        break;
+    }
     if constexpr (T > 1) group_bar<T>(g);  // red reusable
   }
 }
 
 // ============================================================== SUS: one dependency level
+template <int Q, int KR, int DMAX, int DVMAX, bool MARKOV, int S, int G>
+struct SUSShape {
+  static constexpr int T = Q / KR;
+  static constexpr int XR = Extra<Q, MARKOV>::rows;
+  static constexpr size_t PAY = ((size_t)(DMAX - 1) * Q + XR) * 128;
+  static constexpr size_t FWD_D = T > 1 ? (size_t)(DMAX - 1) * Q * 32 : 0;
+  static constexpr size_t ACC_D = T > 1 ? (size_t)Q * 32 : 0;
+  static constexpr size_t RED_D = (size_t)(DVMAX + 2) * T * 32 + (size_t)(DVMAX + 2) * 32 + T * 32;
+  static constexpr size_t RSM_F = (size_t)DVMAX * Q * 32;
+  static constexpr size_t SCR = (FWD_D + ACC_D + RED_D) * 8 + RSM_F * 4;
+  using Sh = Shape<Q, S, G, PAY, SCR>;
+  static constexpr size_t SMEM = Sh::SMEM;
+  static constexpr int THREADS = (1 + G * T) * 32;
+};
+
 // Units: one per (column, check slot) -- the check's other edges in at most
 // two contiguous runs; the last unit of a column also carries the prior's
 // extra rows and the column's VarDesc.
 template <int Q, int DMAX, bool MARKOV>
-__device__ __forceinline__ void sus_issue(const WaveArgs &a, long long task, int s, int lvl_begin, int ncols,
-                                          unsigned char *sb, uint64_t *full, int &nunits_out) {
+__device__ __forceinline__ bool sus_issue(const WaveArgs &a, long long task, int &s, int lvl_begin, int ncols,
+                                          unsigned char *hdr, unsigned char *pay, uint64_t *full) {
   const int fb = a.list[task / ncols];
   const LvlCol lc = a.c.lvl_col[lvl_begin + (int)(task % ncols)];
   const int nunits = lc.dv > 0 ? lc.dv : 1;
-  nunits_out = nunits;
   const LvlUnit un = a.c.lvl_unit[lc.unit0 + s];
-  TaskInfo *ti = (TaskInfo *)sb;
+  TaskInfo *ti = (TaskInfo *)hdr;
   ti->fb = fb; ti->item = lc.j; ti->e0 = lc.e0; ti->deg = lc.dv;
   ti->s = s; ti->r0 = un.r0; ti->d = un.d; ti->pos = un.pos; ti->i = un.i;
   const bool last = (s == nunits - 1);
@@ -786,176 +916,219 @@ __device__ __forceinline__ void sus_issue(const WaveArgs &a, long long task, int
   const uint32_t bx = last ? 64 + extras_bytes<Q, MARKOV>(a, lc.j) : 0;
   mbar_expect_tx(full, (lc.dv > 0 ? 64 + 32 : 0) + (a.early_exit ? 128 : 0) + b0 + b1 + bx);
   if (lc.dv > 0) {
-    bulk_g2s(sb + 128, a.c.sus_desc + lc.e0 + s, 64, full);
-    bulk_g2s(sb + 256, a.z + ((size_t)fb * a.c.M + un.i) * 32, 32, full);
+    bulk_g2s(hdr + 128, a.c.sus_desc + lc.e0 + s, 64, full);
+    bulk_g2s(hdr + 256, a.z + ((size_t)fb * a.c.M + un.i) * 32, 32, full);
   }
-  if (a.early_exit) bulk_g2s(sb + 384, a.conv + fb * 32, 128, full);
-  if (b0) bulk_g2s(sb + kHdr, rowbase, b0, full);
-  if (b1) bulk_g2s(sb + kHdr + (size_t)un.pos * Q * 128, rowbase + (size_t)(un.pos + 1) * Q * 32, b1, full);
+  if (a.early_exit) bulk_g2s(hdr + 384, a.conv + fb * 32, 128, full);
+  if (b0) bulk_g2s(pay, rowbase, b0, full);
+  if (b1) bulk_g2s(pay + (size_t)un.pos * Q * 128, rowbase + (size_t)(un.pos + 1) * Q * 32, b1, full);
   if (last) {
-    bulk_g2s(sb + 192, a.c.var_desc + lc.j, 64, full);
-    issue_extras<Q, MARKOV>(a, fb, lc.j, sb + kHdr + (size_t)(DMAX - 1) * Q * 128, full);
+    bulk_g2s(hdr + 192, a.c.var_desc + lc.j, 64, full);
+    issue_extras<Q, MARKOV>(a, fb, lc.j, pay + (size_t)(DMAX - 1) * Q * 128, full);
+  }
+  if (++s >= nunits) {
+    s = 0;
+    return true;  // task complete
+  }
+  return false;
+}
+
+// Step 1 of SUS for one check (exact number of other edges DO): r_ij from the
+// CURRENT q's of the check's other edges (the transform of k_cn restricted to
+// one output).  Writes q * r_ij into rsm slot s in natural order a.
+template <int Q, int KR, int DO>
+__device__ __forceinline__ void sus_check(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_u32,
+                                          uint64_t *empty, bool release, double *fwd, double *accs, float *rsm,
+                                          int g, int c, int lane, bool frozen) {
+  using C = QC<Q, KR>;
+  constexpr int T = C::T, LKR = C::LKR, LT = C::LT, P = C::P;
+  const TaskInfo ti = *(const TaskInfo *)hdr;
+  const SusDesc *sd = (const SusDesc *)(hdr + 128);
+  const int z = hdr[256 + lane];
+  double v[DO > 0 ? DO : 1][KR];
+#pragma unroll
+  for (int t = 0; t < DO; ++t) {
+    uint32_t ad[KR];
+    int rh;
+    perm_addrs<P, LKR, KR>(pay_u32 + (uint32_t)(t * Q * 128 + lane * 4), sd->perm_o[t], c, ad, rh);
+#pragma unroll
+    for (int k = 0; k < KR; ++k) v[t][k] = (double)lds_f32(ad[k]);
+  }
+  const unsigned long long pke = sd->perm_e;
+  if (release) release_stage(empty, lane);
+#pragma unroll
+  for (int t = 0; t < DO; ++t) wht_bits<KR, 0, LKR>(v[t]);
+  if constexpr (T > 1) {
+#pragma unroll
+    for (int t = 0; t < DO; ++t)
+#pragma unroll
+      for (int k = 0; k < KR; ++k) fwd[((size_t)t * Q + c * KR + k) * 32 + lane] = v[t][k];
+    group_bar<T>(g);
+#pragma unroll
+    for (int t = 0; t < DO; ++t) {
+#pragma unroll
+      for (int k = 0; k < KR; ++k) v[t][k] = fwd[((size_t)t * Q + k * T + c) * 32 + lane];
+      wht_bits<KR, LKR - LT, LKR>(v[t]);
+    }
+  }
+  uint32_t sm[KR];
+  sign_masks<KR, T>(z, c, sm);
+  double acc[KR];
+#pragma unroll
+  for (int k = 0; k < KR; ++k) {
+    double x = 1.0;
+#pragma unroll
+    for (int t = 0; t < DO; ++t) x = (t == 0) ? v[0][k] : x * v[t][k];
+    acc[k] = flip(x, sm[k]);
+  }
+  if constexpr (T > 1) {
+    wht_bits<KR, LKR - LT, LKR>(acc);
+#pragma unroll
+    for (int k = 0; k < KR; ++k) accs[((size_t)k * T + c) * 32 + lane] = acc[k];
+    group_bar<T>(g);
+#pragma unroll
+    for (int k = 0; k < KR; ++k) acc[k] = accs[((size_t)c * KR + k) * 32 + lane];
+  }
+  wht_bits<KR, 0, LKR>(acc);
+  int bbe[P];
+  unpack_basis<P>(pke, bbe);
+  const int rch = row_hi<P, LKR>(bbe, c);
+  const int s = ti.s;
+  float *rdst = (a.rmsg && !frozen) ? a.rmsg + ((size_t)ti.fb * a.c.E + ti.e0 + s) * Q * 32 + lane : nullptr;
+#pragma unroll
+  for (int k = 0; k < KR; ++k) {
+    const float fv = fmaxf((float)acc[k], 0.0f);
+    const int row = rch ^ row_lo<P, LKR>(bbe, k);  // a = h_e^-1 y
+    rsm[((size_t)s * Q + row) * 32 + lane] = fv;
+    if (rdst) rdst[row * 32] = fv;
   }
 }
 
+template <int Q, int KR, int DV, int DVMAX, bool MARKOV>
+__device__ __forceinline__ void sus_vn(const WaveArgs &a, const unsigned char *hdr, const unsigned char *pay,
+                                       int DO_off, uint64_t *empty, const float *rsm, double *red, int g, int c,
+                                       int lane, bool frozen) {
+  const TaskInfo ti = *(const TaskInfo *)hdr;
+  const VarDesc *vd = (const VarDesc *)(hdr + 192);
+  int qdst[DV > 0 ? DV : 1];
+  double r[DV > 0 ? DV : 1][KR];
+#pragma unroll
+  for (int s = 0; s < DV; ++s) {
+    qdst[s] = vd->qdst[s];
+#pragma unroll
+    for (int k = 0; k < KR; ++k) r[s][k] = (double)rsm[((size_t)s * Q + c * KR + k) * 32 + lane];
+  }
+  double pr[KR];
+  prior_from<Q, KR, MARKOV>(a, ti.item, c, lane, (const float *)pay + (size_t)DO_off * Q * 32, pr);
+  release_stage(empty, lane);
+  vn_core<Q, KR, DV, MARKOV>(a, ti.fb, ti.item, qdst, r, pr, red, g, c, lane, frozen);
+}
+
 // For every column j of the level (SUS step 1): r_ij for each
-// check i of column j from the CURRENT q's of check i's other edges (Eq. 3,
-// the transform of k_cn restricted to one output); then (step 2)
-// the vertical update of column j (Eq. 4) and its posterior (step 4, A8).
-// Columns of one level share no check, so they run concurrently with exactly
-// the reads of the serial sweep.
+// check i of column j from the CURRENT q's of check i's other edges; then
+// (step 2) the vertical update of column j (Eq. 4) and its
+// posterior (step 4, A8).  Columns of one level share no check, so they run
+// concurrently with exactly the reads of the serial sweep.
 template <int Q, int KR, int DMAX, int DVMAX, bool MARKOV, int S, int G>
 __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::THREADS)
     k_sus(WaveArgs a, int lvl_begin, int ncols) {
-  using Sh = SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>;
-  using C = QC<Q, KR>;
-  constexpr int T = C::T, LKR = C::LKR, LT = C::LT, P = C::P;
+  using SS = SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>;
+  using Sh = typename SS::Sh;
+  constexpr int T = SS::T;
   constexpr int DO = DMAX - 1;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t *bars = (uint64_t *)smem;
-  unsigned char *stages = smem + Sh::BARS_B;
+  const SmemPtrs sp = smem_ptrs<Sh, S, G>(smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) init_bars<S, G>(bars, T);
+  if (threadIdx.x == 0) init_bars<S, G>(sp.bars, T);
   __syncthreads();
-  const long long E = a.c.E;
   const long long ntask = (long long)(*a.nactive) * ncols;
-  const long long ngroups = (long long)gridDim.x * G;
-  if (warp == 0) {  // ---------------- producer: walks (task, unit) per group
-    if (lane != 0) return;
-    long long t[G], hi[G];
-    int ring[G], su[G], nu[G];
+  if (warp == 0) {
+    if (lane == 0) {
+      int su[G];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      group_range(ntask, (long long)blockIdx.x * G + g, ngroups, t[g], hi[g]);
-      ring[g] = 0;
-      su[g] = 0;
-      nu[g] = 1;
-    }
-    for (bool any = true; any;) {
-      any = false;
+      for (int g = 0; g < G; ++g) su[g] = 0;
+      produce<S, G>(sp.bars, ntask, [&](int g, int st, long long task) {
+        const int k = g * S + st;
+        int s = 0;
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        if (t[g] >= hi[g]) continue;
-        any = true;
-        const int st = ring[g] % S, u = ring[g] / S;
-        if (u > 0 && !mbar_test(bars + G * S + g * S + st, (u - 1) & 1)) continue;
-        sus_issue<Q, DMAX, MARKOV>(a, t[g], su[g], lvl_begin, ncols, stages + (size_t)(g * S + st) * Sh::STAGE_B,
-                                   bars + g * S + st, nu[g]);
-        ++ring[g];
-        if (++su[g] >= nu[g]) {
-          su[g] = 0;
-          ++t[g];
-        }
-      }
+        for (int gg = 0; gg < G; ++gg)
+          if (gg == g) s = su[gg];
+        const bool done = sus_issue<Q, DMAX, MARKOV>(a, task, s, lvl_begin, ncols, sp.hdr + (size_t)k * kHdr,
+                                                     sp.pay + (size_t)k * Sh::PAYA, sp.bars + k);
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg)
+          if (gg == g) su[gg] = s;
+        return done;
+      });
     }
     return;
   }
   const int cw = warp - 1, g = cw / T, c = cw % T;
-  unsigned char *scr = stages + (size_t)G * S * Sh::STAGE_B + (size_t)g * Sh::SCR_B;
+  unsigned char *scr = sp.scr + (size_t)g * SS::SCR;
   double *fwd = (double *)scr;
-  double *accs = fwd + Sh::FWD_D;
-  double *red = accs + Sh::ACC_D;
-  float *rsm = (float *)(red + Sh::RED_D);
+  double *accs = fwd + SS::FWD_D;
+  double *red = accs + SS::ACC_D;
+  float *rsm = (float *)(red + SS::RED_D);
   long long lo, hi;
-  group_range(ntask, (long long)blockIdx.x * G + g, ngroups, lo, hi);
+  group_range(ntask, (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
   int rr = 0;  // units consumed by this group
   for (long long task = lo; task < hi; ++task) {
     int nunits = 1;
 #pragma unroll 1
     for (int s = 0; s < nunits; ++s, ++rr) {
-      const int st = rr % S;
-      unsigned char *sb = stages + (size_t)(g * S + st) * Sh::STAGE_B;
-      uint64_t *empty = bars + G * S + g * S + st;
-      mbar_wait(bars + g * S + st, (uint32_t)((rr / S) & 1));
-      const TaskInfo ti = *(const TaskInfo *)sb;
-      const int fb = ti.fb, j = ti.item, dv = ti.deg;
+      const int st = rr % S, k = g * S + st;
+      const unsigned char *hdr = sp.hdr + (size_t)k * kHdr;
+      const unsigned char *pay = sp.pay + (size_t)k * Sh::PAYA;
+      const uint32_t pay_u32 = sp.pay_u32 + (uint32_t)((size_t)k * Sh::PAYA);
+      uint64_t *empty = sp.bars + G * S + k;
+      mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
+      const TaskInfo *ti = (const TaskInfo *)hdr;
+      const int dv = ti->deg, d = ti->d;
       nunits = dv > 0 ? dv : 1;
       const bool last = (s == nunits - 1);
-      const bool frozen = a.early_exit && ((const int *)(sb + 384))[lane] != 0;
+      const bool frozen = a.early_exit && ((const int *)(hdr + 384))[lane] != 0;
       if (dv > 0) {
-        const SusDesc *sd = (const SusDesc *)(sb + 128);
-        const int d = ti.d;
-        const int z = sb[256 + lane];
-        const float *in = (const float *)(sb + kHdr) + lane;
-        int bbe[P];
-        unpack_basis<P>(sd->perm_e, bbe);
-        double v[DO > 0 ? DO : 1][KR];
-#pragma unroll
-        for (int t = 0; t < DO; ++t) {
-          if (t < d - 1) {
-            int bb[P];
-            unpack_basis<P>(sd->perm_o[t], bb);
-            const int rch = row_hi<P, LKR>(bb, c);
-#pragma unroll
-            for (int k = 0; k < KR; ++k) v[t][k] = (double)in[(t * Q + (rch ^ row_lo<P, LKR>(bb, k))) * 32];
-          }
-        }
-        if (!last) release_stage(empty, lane);
-#pragma unroll
-        for (int t = 0; t < DO; ++t)
-          if (t < d - 1) wht_bits<KR, 0, LKR>(v[t]);
-        if constexpr (T > 1) {
-#pragma unroll
-          for (int t = 0; t < DO; ++t)
-            if (t < d - 1)
-#pragma unroll
-              for (int k = 0; k < KR; ++k) fwd[((size_t)t * Q + c * KR + k) * 32 + lane] = v[t][k];
-          group_bar<T>(g);
-#pragma unroll
-          for (int t = 0; t < DO; ++t)
-            if (t < d - 1) {
-#pragma unroll
-              for (int k = 0; k < KR; ++k) v[t][k] = fwd[((size_t)t * Q + k * T + c) * 32 + lane];
-              wht_bits<KR, LKR - LT, LKR>(v[t]);
+        switch (d - 1) {
+          case 0: sus_check<Q, KR, 0>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen); break;
+          case 1: sus_check<Q, KR, 1>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen); break;
+          case 2: sus_check<Q, KR, 2>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen); break;
+          default:
+            if constexpr (DO <= 3) {
+              sus_check<Q, KR, 3>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen);
+            } else {
+              switch (d - 1) {
+                case 3: sus_check<Q, KR, 3>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen); break;
+                case 4: sus_check<Q, KR, 4>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen); break;
+                case 5: sus_check<Q, KR, 5>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen); break;
+                case 6: sus_check<Q, KR, 6>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen); break;
+                default: sus_check<Q, KR, 7>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen); break;
+              }
             }
-        }
-        double acc[KR];
-#pragma unroll
-        for (int k = 0; k < KR; ++k) {
-          double x = 1.0;
-#pragma unroll
-          for (int t = 0; t < DO; ++t)
-            if (t < d - 1) x *= v[t][k];
-          const int w = (T > 1) ? (k * T + c) : k;
-          acc[k] = neg_if(x, __popc(w & z) & 1);
-        }
-        if constexpr (T > 1) {
-          wht_bits<KR, LKR - LT, LKR>(acc);
-#pragma unroll
-          for (int k = 0; k < KR; ++k) accs[((size_t)k * T + c) * 32 + lane] = acc[k];
-          group_bar<T>(g);
-#pragma unroll
-          for (int k = 0; k < KR; ++k) acc[k] = accs[((size_t)c * KR + k) * 32 + lane];
-        }
-        wht_bits<KR, 0, LKR>(acc);
-        const int rch = row_hi<P, LKR>(bbe, c);
-        float *rdst = (a.rmsg && !frozen) ? a.rmsg + ((size_t)fb * E + ti.e0 + s) * Q * 32 + lane : nullptr;
-#pragma unroll
-        for (int k = 0; k < KR; ++k) {
-          const double x = acc[k] * (1.0 / Q);
-          const float fv = (float)(x > 0.0 ? x : 0.0);
-          const int row = rch ^ row_lo<P, LKR>(bbe, k);  // a = h_e^-1 y
-          rsm[((size_t)s * Q + row) * 32 + lane] = fv;
-          if (rdst) rdst[row * 32] = fv;
+            break;
         }
       }
       if (last) {
         // vertical update of column j from the fresh r's (SUS step 2)
         group_bar<T>(g);  // rsm complete
-        const VarDesc *vd = (const VarDesc *)(sb + 192);
-        int qdst[DVMAX];
-        double r[DVMAX][KR];
-#pragma unroll
-        for (int ss = 0; ss < DVMAX; ++ss)
-          if (ss < dv) {
-            qdst[ss] = vd->qdst[ss];
-#pragma unroll
-            for (int k = 0; k < KR; ++k) r[ss][k] = (double)rsm[((size_t)ss * Q + c * KR + k) * 32 + lane];
-          }
-        double pr[KR];
-        prior_from<Q, KR, MARKOV>(a, j, c, lane, (const float *)(sb + kHdr) + (size_t)DO * Q * 32, pr);
-        release_stage(empty, lane);
-        vn_body<Q, KR, DVMAX, MARKOV>(a, fb, j, dv, qdst, r, pr, red, g, c, lane, frozen);
+        switch (dv) {
+          case 0: sus_vn<Q, KR, 0, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
+          case 1: sus_vn<Q, KR, 1, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
+          case 2: sus_vn<Q, KR, 2, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
+          default:
+            if constexpr (DVMAX <= 3) {
+              sus_vn<Q, KR, 3, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen);
+            } else {
+              switch (dv) {
+                case 3: sus_vn<Q, KR, 3, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
+                case 4: sus_vn<Q, KR, 4, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
+                case 5: sus_vn<Q, KR, 5, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
+                case 6: sus_vn<Q, KR, 6, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
+                case 7: sus_vn<Q, KR, 7, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
+                default: sus_vn<Q, KR, 8, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
+              }
+            }
+            break;
+        }
       }
       group_bar<T>(g);  // transpose / reduction scratch and rsm free
     }
@@ -991,16 +1164,22 @@ static int too_big(const char *what) {
   return GFQ_EUNSUPPORTED;
 }
 
+// stage count that fits: SMEM(S) = SMEM(1) + (S-1)*G*PAYA (+ headers)
+template <typename S1, typename S2>
+constexpr int stages_fit(int want) {
+  return (S1::SMEM + (size_t)(want - 1) * (S2::SMEM - S1::SMEM) <= 232448 || want <= 1) ? want
+                                                                                       : stages_fit<S1, S2>(want - 1);
+}
+
 template <int Q, int DM>
 static int cn_launch(const WaveArgs &a, cudaStream_t s) {
   constexpr int KR = KRof<Q, KCN>::v, T = Q / KR, G = Gof<T>::v;
-  using S1 = CNShape<Q, KR, DM, 1, G>;
-  constexpr int NS = fit_stages(G * S1::STAGE_B, S1::BARS_B + G * S1::SCR_B, GFQ_STAGES_CN);
-  using Sh = CNShape<Q, KR, DM, NS, G>;
-  if (Sh::SMEM > 232448) return too_big("k_cn");
+  constexpr int NS = stages_fit<CNShape<Q, KR, DM, 1, G>, CNShape<Q, KR, DM, 2, G>>(GFQ_STAGES_CN);
+  using CS = CNShape<Q, KR, DM, NS, G>;
+  if (CS::SMEM > 232448) return too_big("k_cn");
   auto k = k_cn<Q, KR, DM, NS, G>;
-  const int grid = grid_for(k, Sh::THREADS, Sh::SMEM, ((long long)a.nfb * a.c.M + G - 1) / G);
-  k<<<grid, Sh::THREADS, Sh::SMEM, s>>>(a);
+  const int grid = grid_for(k, CS::THREADS, CS::SMEM, ((long long)a.nfb * a.c.M + G - 1) / G);
+  k<<<grid, CS::THREADS, CS::SMEM, s>>>(a);
   return check_launch("k_cn");
 }
 
@@ -1012,13 +1191,12 @@ static int cn_q(const WaveArgs &a, cudaStream_t s) {
 template <int Q, int DV, bool MK>
 static int vn_launch(const WaveArgs &a, int clip, cudaStream_t s) {
   constexpr int KR = KRof<Q, KVN>::v, T = Q / KR, G = Gof<T>::v;
-  using S1 = VNShape<Q, KR, DV, MK, 1, G>;
-  constexpr int NS = fit_stages(G * S1::STAGE_B, S1::BARS_B + G * S1::SCR_B, GFQ_STAGES_VN);
-  using Sh = VNShape<Q, KR, DV, MK, NS, G>;
-  if (Sh::SMEM > 232448) return too_big("k_vn");
+  constexpr int NS = stages_fit<VNShape<Q, KR, DV, MK, 1, G>, VNShape<Q, KR, DV, MK, 2, G>>(GFQ_STAGES_VN);
+  using VS = VNShape<Q, KR, DV, MK, NS, G>;
+  if (VS::SMEM > 232448) return too_big("k_vn");
   auto k = k_vn<Q, KR, DV, MK, NS, G>;
-  const int grid = grid_for(k, Sh::THREADS, Sh::SMEM, ((long long)a.nfb * a.c.V + G - 1) / G);
-  k<<<grid, Sh::THREADS, Sh::SMEM, s>>>(a, clip);
+  const int grid = grid_for(k, VS::THREADS, VS::SMEM, ((long long)a.nfb * a.c.V + G - 1) / G);
+  k<<<grid, VS::THREADS, VS::SMEM, s>>>(a, clip);
   return check_launch("k_vn");
 }
 
@@ -1032,13 +1210,13 @@ static int vn_q(const WaveArgs &a, int clip, cudaStream_t s) {
 template <int Q, int DM, int DV, bool MK>
 static int sus_launch(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
   constexpr int KR = KRof<Q, KSUS>::v, T = Q / KR, G = Gof<T>::v;
-  using S1 = SUSShape<Q, KR, DM, DV, MK, 1, G>;
-  constexpr int NS = fit_stages(G * S1::STAGE_B, S1::BARS_B + G * S1::SCR_B, GFQ_STAGES_SUS);
-  using Sh = SUSShape<Q, KR, DM, DV, MK, NS, G>;
-  if (Sh::SMEM > 232448) return too_big("k_sus");
+  constexpr int NS =
+      stages_fit<SUSShape<Q, KR, DM, DV, MK, 1, G>, SUSShape<Q, KR, DM, DV, MK, 2, G>>(GFQ_STAGES_SUS);
+  using SS = SUSShape<Q, KR, DM, DV, MK, NS, G>;
+  if (SS::SMEM > 232448) return too_big("k_sus");
   auto k = k_sus<Q, KR, DM, DV, MK, NS, G>;
-  const int grid = grid_for(k, Sh::THREADS, Sh::SMEM, ((long long)a.nfb * ncols + G - 1) / G);
-  k<<<grid, Sh::THREADS, Sh::SMEM, s>>>(a, lb, ncols);
+  const int grid = grid_for(k, SS::THREADS, SS::SMEM, ((long long)a.nfb * ncols + G - 1) / G);
+  k<<<grid, SS::THREADS, SS::SMEM, s>>>(a, lb, ncols);
   return check_launch("k_sus");
 }
 

@@ -251,7 +251,7 @@ __global__ void k_compact(WaveArgs a, unsigned int *host_count) {
 __global__ void k_set_u64(unsigned long long *p, unsigned long long v) { *p = v; }
 
 // Export to [frame][canonical edge][q] / [frame][V][q] (debug and parity only).
-__global__ void k_export(WaveArgs a, const float *src, float *dst, int items, const int *map) {
+__global__ void k_export(WaveArgs a, const float *src, float *dst, int items, const int *map, float scale) {
   const int q = a.c.q;
   const long long n = (long long)a.nfb * 32 * items * q;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
@@ -263,7 +263,7 @@ __global__ void k_export(WaveArgs a, const float *src, float *dst, int items, co
     if (gf >= a.n_frames) continue;
     const int fb = (int)(f >> 5), lane = (int)(f & 31);
     const int it = map ? map[item] : item;
-    dst[(gf * items + item) * q + x] = src[(((size_t)fb * items + it) * q + x) * 32 + lane];
+    dst[(gf * items + item) * q + x] = scale * src[(((size_t)fb * items + it) * q + x) * 32 + lane];
   }
 }
 
@@ -325,9 +325,10 @@ int launch_export(const WaveArgs &a, float *q_out, float *r_out, float *Q_out, c
   const int threads = 256;
   const int grid = sm_count() * 8;
   // q messages live in check-major edge order, r messages in canonical order
-  if (q_out) k_export<<<grid, threads, 0, s>>>(a, a.qmsg, q_out, (int)a.c.E, a.c.col_edge);
-  if (r_out) k_export<<<grid, threads, 0, s>>>(a, a.rmsg, r_out, (int)a.c.E, nullptr);
-  if (Q_out) k_export<<<grid, threads, 0, s>>>(a, a.qall, Q_out, a.c.V, nullptr);
+  // (r is stored as q * r: the kernels drop the 1/q of the inverse transform)
+  if (q_out) k_export<<<grid, threads, 0, s>>>(a, a.qmsg, q_out, (int)a.c.E, a.c.col_edge, 1.0f);
+  if (r_out) k_export<<<grid, threads, 0, s>>>(a, a.rmsg, r_out, (int)a.c.E, nullptr, 1.0f / a.c.q);
+  if (Q_out) k_export<<<grid, threads, 0, s>>>(a, a.qall, Q_out, a.c.V, nullptr, 1.0f);
   return check_launch("k_export");
 }
 
