@@ -80,9 +80,12 @@ constexpr int fit_stages(size_t per_stage, size_t other, int max_s) {
 }
 
 // groups per CTA for a given number of warps per group
+#ifndef GFQ_G_T8
+#define GFQ_G_T8 2
+#endif
 template <int T>
 struct Gof {
-  static constexpr int v = T >= 8 ? 1 : (4 / T > 0 ? 4 / T : 1);
+  static constexpr int v = T >= 8 ? GFQ_G_T8 : (4 / T > 0 ? 4 / T : 1);
 };
 
 // ============================================================== PTX: mbarrier + TMA bulk copy
@@ -537,21 +540,75 @@ __device__ __forceinline__ void vn_core(const WaveArgs &a, int fb, int j, const 
   }
 }
 
+
+// ============================================================== layout switches (T > 1)
+// Layout A -> B (or B -> A) of D messages through shared memory.  Bulk mode
+// (PP = false): one buffer per message, one barrier for all of them; the
+// caller separates successive uses with a barrier.  Ping-pong mode (PP = true,
+// large q): two message buffers used alternately, one barrier per message and
+// no other barrier needed -- the counter m (same in every warp of the group)
+// carries the alternation across calls and tasks.
+template <int Q, int KR>
+__device__ __forceinline__ int idxA(int c, int k) { return c * KR + k; }
+template <int Q, int KR>
+__device__ __forceinline__ int idxB(int c, int k) { return k * (Q / KR) + c; }
+
+template <int Q, int KR, int D, bool PP, bool A2B>
+__device__ __forceinline__ void xpose(double (&u)[D][KR], double *buf, int &m, int g, int c, int lane) {
+  constexpr int T = Q / KR;
+  if constexpr (!PP) {
+#pragma unroll
+    for (int s = 0; s < D; ++s)
+#pragma unroll
+      for (int k = 0; k < KR; ++k)
+        buf[((size_t)s * Q + (A2B ? idxA<Q, KR>(c, k) : idxB<Q, KR>(c, k))) * 32 + lane] = u[s][k];
+    group_bar<T>(g);
+#pragma unroll
+    for (int s = 0; s < D; ++s)
+#pragma unroll
+      for (int k = 0; k < KR; ++k)
+        u[s][k] = buf[((size_t)s * Q + (A2B ? idxB<Q, KR>(c, k) : idxA<Q, KR>(c, k))) * 32 + lane];
+  } else {
+#pragma unroll
+    for (int s = 0; s < D; ++s) {
+      double *b = buf + (size_t)(m & 1) * Q * 32;
+      ++m;
+#pragma unroll
+      for (int k = 0; k < KR; ++k) b[(A2B ? idxA<Q, KR>(c, k) : idxB<Q, KR>(c, k)) * 32 + lane] = u[s][k];
+      group_bar<T>(g);
+#pragma unroll
+      for (int k = 0; k < KR; ++k) u[s][k] = b[(A2B ? idxB<Q, KR>(c, k) : idxA<Q, KR>(c, k)) * 32 + lane];
+    }
+  }
+}
+
+// ping-pong transposes for large fields (tuning knob)
+#ifndef GFQ_PP_MINQ
+#define GFQ_PP_MINQ 32
+#endif
+template <int Q>
+struct PPof {
+  static constexpr bool v = Q >= GFQ_PP_MINQ;
+};
+
 // ============================================================== shared-memory layout
 // [mbarriers][G*S headers of kHdr][pad][G*S payload slots, each a multiple of
 // PAL = q*128 bytes and PAL-aligned in the shared window][G scratch areas]
-template <int Q, int S, int G, size_t PAY, size_t SCR>
+template <int Q, int S, int G, size_t PAY, size_t SCR, size_t XTRA = 0>
 struct Shape {
   static constexpr size_t PAL = (size_t)Q * 128;
   static constexpr size_t PAYA = ((PAY + PAL - 1) / PAL) * PAL;
   static constexpr size_t BARS_B = ((16 * S * G + 127) / 128) * 128;
   static constexpr size_t HDR_B = (size_t)G * S * kHdr;
-  static constexpr size_t SMEM = BARS_B + HDR_B + PAL + (size_t)G * S * PAYA + (size_t)G * SCR;
+  static constexpr size_t XTRA_A = ((XTRA + 127) / 128) * 128;
+  static constexpr size_t XTRA_B = (size_t)G * S * XTRA_A;
+  static constexpr size_t SMEM = BARS_B + HDR_B + XTRA_B + PAL + (size_t)G * S * PAYA + (size_t)G * SCR;
 };
 
 struct SmemPtrs {
   uint64_t *bars;
   unsigned char *hdr;
+  unsigned char *xtra;
   unsigned char *pay;
   uint32_t pay_u32;
   unsigned char *scr;
@@ -562,8 +619,9 @@ __device__ __forceinline__ SmemPtrs smem_ptrs(unsigned char *smem) {
   SmemPtrs p;
   p.bars = (uint64_t *)smem;
   p.hdr = smem + Sh::BARS_B;
+  p.xtra = p.hdr + Sh::HDR_B;
   const uint32_t base = smem_u32(smem);
-  const uint32_t want = base + (uint32_t)(Sh::BARS_B + Sh::HDR_B);
+  const uint32_t want = base + (uint32_t)(Sh::BARS_B + Sh::HDR_B + Sh::XTRA_B);
   const uint32_t al = (uint32_t)(((want + Sh::PAL - 1) / Sh::PAL) * Sh::PAL);
   p.pay = smem + (al - base);
   p.pay_u32 = al;
@@ -595,15 +653,25 @@ __device__ __forceinline__ void produce(uint64_t *bars, long long ntask, Issue i
   }
   for (bool any = true; any;) {
     any = false;
+    bool did = false;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       if (t[g] >= hi[g]) continue;
       any = true;
       const int st = ring[g] % S, u = ring[g] / S;
-      if (u > 0 && !mbar_test(bars + G * S + g * S + st, (u - 1) & 1)) continue;
+      if (u > 0) {
+        uint64_t *empty = bars + G * S + g * S + st;
+        if (G == 1) {
+          mbar_wait(empty, (u - 1) & 1);  // hardware-suspended wait
+        } else if (!mbar_test(empty, (u - 1) & 1)) {
+          continue;
+        }
+      }
       if (issue(g, st, t[g])) ++t[g];
       ++ring[g];
+      did = true;
     }
+    if (!did && any) __nanosleep(64);  // leave the issue slots to the consumers
   }
 }
 
@@ -611,8 +679,9 @@ __device__ __forceinline__ void produce(uint64_t *bars, long long ntask, Issue i
 template <int Q, int KR, int DMAX, int S, int G>
 struct CNShape {
   static constexpr int T = Q / KR;
+  static constexpr bool PP = PPof<Q>::v;
   static constexpr size_t PAY = (size_t)DMAX * Q * 128;
-  static constexpr size_t SCR = T > 1 ? (size_t)DMAX * Q * 32 * 8 : 0;
+  static constexpr size_t SCR = T > 1 ? (size_t)(PP ? 2 : DMAX) * Q * 32 * 8 : 0;
   using Sh = Shape<Q, S, G, PAY, SCR>;
   static constexpr size_t SMEM = Sh::SMEM;
   static constexpr int THREADS = (1 + G * T) * 32;
@@ -645,42 +714,36 @@ __device__ __forceinline__ void cn_issue(const WaveArgs &a, long long task, unsi
 // round-off is clamped to 0 (reading A20).
 template <int Q, int KR, int D, int DMAX>
 __device__ __forceinline__ void cn_task(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_u32,
-                                        uint64_t *empty, double *xp, int g, int c, int lane) {
+                                        uint64_t *empty, double *xp, int &m, int g, int c, int lane) {
   using C = QC<Q, KR>;
   constexpr int T = C::T, LKR = C::LKR, LT = C::LT, P = C::P;
+  constexpr bool PP = PPof<Q>::v;
   const TaskInfo ti = *(const TaskInfo *)hdr;
   const CheckDesc *cd = (const CheckDesc *)(hdr + 128);
   const int fb = ti.fb;
   const int z = hdr[256 + lane];
   const bool frozen = a.early_exit && ((const int *)(hdr + 384))[lane] != 0;
   const long long E = a.c.E;
-  uint32_t ad[D][KR];
-  int rh[D];
   double u[D][KR];
-#pragma unroll
-  for (int s = 0; s < D; ++s) {
-    perm_addrs<P, LKR, KR>(pay_u32 + (uint32_t)(s * Q * 128 + lane * 4), cd->perm[s], c, ad[s], rh[s]);
-#pragma unroll
-    for (int k = 0; k < KR; ++k) u[s][k] = (double)lds_f32(ad[s][k]);
-  }
+  unsigned long long pk[D];
   int canon[D];
 #pragma unroll
-  for (int s = 0; s < D; ++s) canon[s] = cd->canon[s];
+  for (int s = 0; s < D; ++s) {
+    pk[s] = cd->perm[s];
+    canon[s] = cd->canon[s];
+    uint32_t ad[KR];
+    int rh;
+    perm_addrs<P, LKR, KR>(pay_u32 + (uint32_t)(s * Q * 128 + lane * 4), pk[s], c, ad, rh);
+#pragma unroll
+    for (int k = 0; k < KR; ++k) u[s][k] = (double)lds_f32(ad[k]);
+  }
   release_stage(empty, lane);
 #pragma unroll
   for (int s = 0; s < D; ++s) wht_bits<KR, 0, LKR>(u[s]);
   if constexpr (T > 1) {
+    xpose<Q, KR, D, PP, true>(u, xp, m, g, c, lane);
 #pragma unroll
-    for (int s = 0; s < D; ++s)
-#pragma unroll
-      for (int k = 0; k < KR; ++k) xp[((size_t)s * Q + c * KR + k) * 32 + lane] = u[s][k];
-    group_bar<T>(g);
-#pragma unroll
-    for (int s = 0; s < D; ++s) {
-#pragma unroll
-      for (int k = 0; k < KR; ++k) u[s][k] = xp[((size_t)s * Q + k * T + c) * 32 + lane];
-      wht_bits<KR, LKR - LT, LKR>(u[s]);
-    }
+    for (int s = 0; s < D; ++s) wht_bits<KR, LKR - LT, LKR>(u[s]);
   }
   uint32_t sm[KR];
   sign_masks<KR, T>(z, c, sm);
@@ -688,32 +751,23 @@ __device__ __forceinline__ void cn_task(const WaveArgs &a, const unsigned char *
   if constexpr (T > 1) {
 #pragma unroll
     for (int s = 0; s < D; ++s) wht_bits<KR, LKR - LT, LKR>(u[s]);
-    group_bar<T>(g);
-#pragma unroll
-    for (int s = 0; s < D; ++s)
-#pragma unroll
-      for (int k = 0; k < KR; ++k) xp[((size_t)s * Q + k * T + c) * 32 + lane] = u[s][k];
-    group_bar<T>(g);
-#pragma unroll
-    for (int s = 0; s < D; ++s)
-#pragma unroll
-      for (int k = 0; k < KR; ++k) u[s][k] = xp[((size_t)s * Q + c * KR + k) * 32 + lane];
-    group_bar<T>(g);
+    if constexpr (!PP) group_bar<T>(g);  // bulk buffer: all forward reads done
+    xpose<Q, KR, D, PP, false>(u, xp, m, g, c, lane);
+    if constexpr (!PP) group_bar<T>(g);  // bulk buffer free for the next task
   }
 #pragma unroll
   for (int s = 0; s < D; ++s) {
     wht_bits<KR, 0, LKR>(u[s]);
     if (!frozen) {
+      // same rows as the load: r_k(a) lands at a = h^-1 y
+      uint32_t ad[KR];
+      int rh;
+      perm_addrs<P, LKR, KR>(0u, pk[s], c, ad, rh);
       unsigned char *dst = (unsigned char *)(a.rmsg + ((size_t)fb * E + canon[s]) * Q * 32 + lane);
 #pragma unroll
-      for (int k = 0; k < KR; ++k) {
-        // same rows as the load: r_k(a) lands at a = h^-1 y
-        const uint32_t roff = (ad[s][k] ^ (pay_u32 + (uint32_t)(s * Q * 128 + lane * 4)));
-        *(float *)(dst + roff) = fmaxf((float)u[s][k], 0.0f);
-      }
+      for (int k = 0; k < KR; ++k) *(float *)(dst + ad[k]) = fmaxf((float)u[s][k], 0.0f);
     }
   }
-  (void)rh;
 }
 
 template <int Q, int KR, int DMAX, int S, int G>
@@ -739,6 +793,7 @@ __global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(Wave
   }
   const int cw = warp - 1, g = cw / T, c = cw % T;
   double *xp = (double *)(sp.scr + (size_t)g * CS::SCR);
+  int m = 0;  // ping-pong transpose counter
   long long lo, hi;
   group_range(ntask, (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
   for (long long task = lo; task < hi; ++task) {
@@ -749,17 +804,17 @@ __global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(Wave
     mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
     const int d = ((const TaskInfo *)hdr)->deg;
     switch (d) {
-      case 1: cn_task<Q, KR, 1, DMAX>(a, hdr, pay, empty, xp, g, c, lane); break;
-      case 2: cn_task<Q, KR, 2, DMAX>(a, hdr, pay, empty, xp, g, c, lane); break;
-      case 3: cn_task<Q, KR, 3, DMAX>(a, hdr, pay, empty, xp, g, c, lane); break;
-      case 4: cn_task<Q, KR, 4, DMAX>(a, hdr, pay, empty, xp, g, c, lane); break;
+      case 1: cn_task<Q, KR, 1, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane); break;
+      case 2: cn_task<Q, KR, 2, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane); break;
+      case 3: cn_task<Q, KR, 3, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane); break;
+      case 4: cn_task<Q, KR, 4, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane); break;
       default:
         if constexpr (DMAX > 4) {
           switch (d) {
-            case 5: cn_task<Q, KR, 5, DMAX>(a, hdr, pay, empty, xp, g, c, lane); break;
-            case 6: cn_task<Q, KR, 6, DMAX>(a, hdr, pay, empty, xp, g, c, lane); break;
-            case 7: cn_task<Q, KR, 7, DMAX>(a, hdr, pay, empty, xp, g, c, lane); break;
-            default: cn_task<Q, KR, 8, DMAX>(a, hdr, pay, empty, xp, g, c, lane); break;
+            case 5: cn_task<Q, KR, 5, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane); break;
+            case 6: cn_task<Q, KR, 6, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane); break;
+            case 7: cn_task<Q, KR, 7, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane); break;
+            default: cn_task<Q, KR, 8, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane); break;
           }
         } else {
           release_stage(empty, lane);  // d == 0: an empty check has no edge
@@ -774,16 +829,16 @@ template <int Q, int KR, int DVMAX, bool MARKOV, int S, int G>
 struct VNShape {
   static constexpr int T = Q / KR;
   static constexpr int XR = Extra<Q, MARKOV>::rows;
-  static constexpr size_t PAY = ((size_t)DVMAX * Q + XR) * 128;
+  static constexpr size_t PAY = (size_t)DVMAX * Q * 128;
   static constexpr size_t SCR = ((size_t)(DVMAX + 2) * T * 32 + (size_t)(DVMAX + 2) * 32 + T * 32) * 8;
-  using Sh = Shape<Q, S, G, PAY, SCR>;
+  using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128>;
   static constexpr size_t SMEM = Sh::SMEM;
   static constexpr int THREADS = (1 + G * T) * 32;
 };
 
 template <int Q, int DVMAX, bool MARKOV>
 __device__ __forceinline__ void vn_issue(const WaveArgs &a, long long task, unsigned char *hdr, unsigned char *pay,
-                                         uint64_t *full, int clip_only) {
+                                         unsigned char *xtra, uint64_t *full, int clip_only) {
   const int V = a.c.V;
   const int fb = a.list[task / V];
   const int j = (int)(task % V);
@@ -796,12 +851,13 @@ __device__ __forceinline__ void vn_issue(const WaveArgs &a, long long task, unsi
   bulk_g2s(hdr + 192, a.c.var_desc + j, 64, full);
   if (a.early_exit) bulk_g2s(hdr + 384, a.conv + fb * 32, 128, full);
   if (br) bulk_g2s(pay, a.rmsg + ((size_t)fb * a.c.E + e0) * Q * 32, br, full);  // canonical order
-  issue_extras<Q, MARKOV>(a, fb, j, pay + (size_t)DVMAX * Q * 128, full);
+  issue_extras<Q, MARKOV>(a, fb, j, xtra, full);
 }
 
 template <int Q, int KR, int DV, int DVMAX, bool MARKOV>
 __device__ __forceinline__ void vn_task(const WaveArgs &a, const unsigned char *hdr, const unsigned char *pay,
-                                        uint64_t *empty, double *red, int g, int c, int lane) {
+                                        const unsigned char *xtra, uint64_t *empty, double *red, int g, int c,
+                                        int lane) {
   const TaskInfo ti = *(const TaskInfo *)hdr;
   const VarDesc *vd = (const VarDesc *)(hdr + 192);
   const bool frozen = a.early_exit && ((const int *)(hdr + 384))[lane] != 0;
@@ -815,7 +871,7 @@ __device__ __forceinline__ void vn_task(const WaveArgs &a, const unsigned char *
     for (int k = 0; k < KR; ++k) r[s][k] = (double)in[(s * Q + k) * 32];
   }
   double pr[KR];
-  prior_from<Q, KR, MARKOV>(a, ti.item, c, lane, (const float *)pay + (size_t)DVMAX * Q * 32, pr);
+  prior_from<Q, KR, MARKOV>(a, ti.item, c, lane, (const float *)xtra, pr);
   release_stage(empty, lane);
   vn_core<Q, KR, DV, MARKOV>(a, ti.fb, ti.item, qdst, r, pr, red, g, c, lane, frozen);
 }
@@ -837,8 +893,8 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
     if (lane == 0)
       produce<S, G>(sp.bars, ntask, [&](int g, int st, long long task) {
         const int k = g * S + st;
-        vn_issue<Q, DVMAX, MARKOV>(a, task, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA, sp.bars + k,
-                                   clip_only);
+        vn_issue<Q, DVMAX, MARKOV>(a, task, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA,
+                                   sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k, clip_only);
         return true;
       });
     return;
@@ -851,24 +907,25 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
     const int rr = (int)(task - lo), st = rr % S, k = g * S + st;
     const unsigned char *hdr = sp.hdr + (size_t)k * kHdr;
     const unsigned char *pay = sp.pay + (size_t)k * Sh::PAYA;
+    const unsigned char *xtra = sp.xtra + (size_t)k * Sh::XTRA_A;
     uint64_t *empty = sp.bars + G * S + k;
     mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
     const int dv = ((const TaskInfo *)hdr)->deg;
     switch (dv) {
-      case 0: vn_task<Q, KR, 0, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
-      case 1: vn_task<Q, KR, 1, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
-      case 2: vn_task<Q, KR, 2, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
+      case 0: vn_task<Q, KR, 0, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
+      case 1: vn_task<Q, KR, 1, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
+      case 2: vn_task<Q, KR, 2, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
       default:
         if constexpr (DVMAX <= 3) {
-          vn_task<Q, KR, 3, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane);
+          vn_task<Q, KR, 3, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane);
         } else {
           switch (dv) {
-            case 3: vn_task<Q, KR, 3, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
-            case 4: vn_task<Q, KR, 4, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
-            case 5: vn_task<Q, KR, 5, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
-            case 6: vn_task<Q, KR, 6, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
-            case 7: vn_task<Q, KR, 7, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
-            default: vn_task<Q, KR, 8, DVMAX, MARKOV>(a, hdr, pay, empty, red, g, c, lane); break;
+            case 3: vn_task<Q, KR, 3, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
+            case 4: vn_task<Q, KR, 4, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
+            case 5: vn_task<Q, KR, 5, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
+            case 6: vn_task<Q, KR, 6, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
+            case 7: vn_task<Q, KR, 7, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
+            default: vn_task<Q, KR, 8, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
           }
         }
         break;
@@ -881,14 +938,17 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
 template <int Q, int KR, int DMAX, int DVMAX, bool MARKOV, int S, int G>
 struct SUSShape {
   static constexpr int T = Q / KR;
+  static constexpr bool PP = PPof<Q>::v;
   static constexpr int XR = Extra<Q, MARKOV>::rows;
-  static constexpr size_t PAY = ((size_t)(DMAX - 1) * Q + XR) * 128;
-  static constexpr size_t FWD_D = T > 1 ? (size_t)(DMAX - 1) * Q * 32 : 0;
-  static constexpr size_t ACC_D = T > 1 ? (size_t)Q * 32 : 0;
+  static constexpr size_t PAY = (size_t)(DMAX - 1) * Q * 128;
+  // transpose buffers (bulk: DMAX-1 forward + 1 accumulator; ping-pong: 2);
+  // the variable-node reduction scratch aliases them (used after the last transpose)
+  static constexpr size_t XP_D = T > 1 ? (size_t)(PP ? 2 : DMAX) * Q * 32 : 0;
   static constexpr size_t RED_D = (size_t)(DVMAX + 2) * T * 32 + (size_t)(DVMAX + 2) * 32 + T * 32;
+  static constexpr size_t XR_D = XP_D > RED_D ? XP_D : RED_D;
   static constexpr size_t RSM_F = (size_t)DVMAX * Q * 32;
-  static constexpr size_t SCR = (FWD_D + ACC_D + RED_D) * 8 + RSM_F * 4;
-  using Sh = Shape<Q, S, G, PAY, SCR>;
+  static constexpr size_t SCR = XR_D * 8 + RSM_F * 4;
+  using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128>;
   static constexpr size_t SMEM = Sh::SMEM;
   static constexpr int THREADS = (1 + G * T) * 32;
 };
@@ -898,7 +958,8 @@ struct SUSShape {
 // extra rows and the column's VarDesc.
 template <int Q, int DMAX, bool MARKOV>
 __device__ __forceinline__ bool sus_issue(const WaveArgs &a, long long task, int &s, int lvl_begin, int ncols,
-                                          unsigned char *hdr, unsigned char *pay, uint64_t *full) {
+                                          unsigned char *hdr, unsigned char *pay, unsigned char *xtra,
+                                          uint64_t *full) {
   const int fb = a.list[task / ncols];
   const LvlCol lc = a.c.lvl_col[lvl_begin + (int)(task % ncols)];
   const int nunits = lc.dv > 0 ? lc.dv : 1;
@@ -924,7 +985,7 @@ __device__ __forceinline__ bool sus_issue(const WaveArgs &a, long long task, int
   if (b1) bulk_g2s(pay + (size_t)un.pos * Q * 128, rowbase + (size_t)(un.pos + 1) * Q * 32, b1, full);
   if (last) {
     bulk_g2s(hdr + 192, a.c.var_desc + lc.j, 64, full);
-    issue_extras<Q, MARKOV>(a, fb, lc.j, pay + (size_t)(DMAX - 1) * Q * 128, full);
+    issue_extras<Q, MARKOV>(a, fb, lc.j, xtra, full);
   }
   if (++s >= nunits) {
     s = 0;
@@ -936,12 +997,13 @@ __device__ __forceinline__ bool sus_issue(const WaveArgs &a, long long task, int
 // Step 1 of SUS for one check (exact number of other edges DO): r_ij from the
 // CURRENT q's of the check's other edges (the transform of k_cn restricted to
 // one output).  Writes q * r_ij into rsm slot s in natural order a.
-template <int Q, int KR, int DO>
+template <int Q, int KR, int DO, int DMAX>
 __device__ __forceinline__ void sus_check(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_u32,
-                                          uint64_t *empty, bool release, double *fwd, double *accs, float *rsm,
-                                          int g, int c, int lane, bool frozen) {
+                                          uint64_t *empty, bool release, double *xp, int &m, float *rsm, int g,
+                                          int c, int lane, bool frozen) {
   using C = QC<Q, KR>;
   constexpr int T = C::T, LKR = C::LKR, LT = C::LT, P = C::P;
+  constexpr bool PP = PPof<Q>::v;
   const TaskInfo ti = *(const TaskInfo *)hdr;
   const SusDesc *sd = (const SusDesc *)(hdr + 128);
   const int z = hdr[256 + lane];
@@ -959,55 +1021,48 @@ __device__ __forceinline__ void sus_check(const WaveArgs &a, const unsigned char
 #pragma unroll
   for (int t = 0; t < DO; ++t) wht_bits<KR, 0, LKR>(v[t]);
   if constexpr (T > 1) {
+    if constexpr (DO > 0) {
+      xpose<Q, KR, DO, PP, true>(v, xp, m, g, c, lane);
 #pragma unroll
-    for (int t = 0; t < DO; ++t)
-#pragma unroll
-      for (int k = 0; k < KR; ++k) fwd[((size_t)t * Q + c * KR + k) * 32 + lane] = v[t][k];
-    group_bar<T>(g);
-#pragma unroll
-    for (int t = 0; t < DO; ++t) {
-#pragma unroll
-      for (int k = 0; k < KR; ++k) v[t][k] = fwd[((size_t)t * Q + k * T + c) * 32 + lane];
-      wht_bits<KR, LKR - LT, LKR>(v[t]);
+      for (int t = 0; t < DO; ++t) wht_bits<KR, LKR - LT, LKR>(v[t]);
     }
   }
   uint32_t sm[KR];
   sign_masks<KR, T>(z, c, sm);
-  double acc[KR];
+  double acc[1][KR];
 #pragma unroll
   for (int k = 0; k < KR; ++k) {
     double x = 1.0;
 #pragma unroll
     for (int t = 0; t < DO; ++t) x = (t == 0) ? v[0][k] : x * v[t][k];
-    acc[k] = flip(x, sm[k]);
+    acc[0][k] = flip(x, sm[k]);
   }
   if constexpr (T > 1) {
-    wht_bits<KR, LKR - LT, LKR>(acc);
-#pragma unroll
-    for (int k = 0; k < KR; ++k) accs[((size_t)k * T + c) * 32 + lane] = acc[k];
-    group_bar<T>(g);
-#pragma unroll
-    for (int k = 0; k < KR; ++k) acc[k] = accs[((size_t)c * KR + k) * 32 + lane];
+    wht_bits<KR, LKR - LT, LKR>(acc[0]);
+    // bulk mode: the accumulator uses its own slot (index DMAX-1) of the buffer
+    xpose<Q, KR, 1, PP, false>(acc, PP ? xp : xp + (size_t)(DMAX - 1) * Q * 32, m, g, c, lane);
   }
-  wht_bits<KR, 0, LKR>(acc);
-  int bbe[P];
-  unpack_basis<P>(pke, bbe);
-  const int rch = row_hi<P, LKR>(bbe, c);
+  wht_bits<KR, 0, LKR>(acc[0]);
+  uint32_t ad[KR];
+  int rh;
+  perm_addrs<P, LKR, KR>(0u, pke, c, ad, rh);  // ad[k] = (h_e^-1 y) * 128: a = h_e^-1 y
   const int s = ti.s;
-  float *rdst = (a.rmsg && !frozen) ? a.rmsg + ((size_t)ti.fb * a.c.E + ti.e0 + s) * Q * 32 + lane : nullptr;
+  unsigned char *rs = (unsigned char *)(rsm + (size_t)s * Q * 32 + lane);
+  unsigned char *rdst =
+      (a.rmsg && !frozen) ? (unsigned char *)(a.rmsg + ((size_t)ti.fb * a.c.E + ti.e0 + s) * Q * 32 + lane)
+                          : nullptr;
 #pragma unroll
   for (int k = 0; k < KR; ++k) {
-    const float fv = fmaxf((float)acc[k], 0.0f);
-    const int row = rch ^ row_lo<P, LKR>(bbe, k);  // a = h_e^-1 y
-    rsm[((size_t)s * Q + row) * 32 + lane] = fv;
-    if (rdst) rdst[row * 32] = fv;
+    const float fv = fmaxf((float)acc[0][k], 0.0f);
+    *(float *)(rs + ad[k]) = fv;
+    if (rdst) *(float *)(rdst + ad[k]) = fv;
   }
 }
 
 template <int Q, int KR, int DV, int DVMAX, bool MARKOV>
-__device__ __forceinline__ void sus_vn(const WaveArgs &a, const unsigned char *hdr, const unsigned char *pay,
-                                       int DO_off, uint64_t *empty, const float *rsm, double *red, int g, int c,
-                                       int lane, bool frozen) {
+__device__ __forceinline__ void sus_vn(const WaveArgs &a, const unsigned char *hdr, const unsigned char *xtra,
+                                       uint64_t *empty, const float *rsm, double *red, int g, int c, int lane,
+                                       bool frozen) {
   const TaskInfo ti = *(const TaskInfo *)hdr;
   const VarDesc *vd = (const VarDesc *)(hdr + 192);
   int qdst[DV > 0 ? DV : 1];
@@ -1019,7 +1074,7 @@ __device__ __forceinline__ void sus_vn(const WaveArgs &a, const unsigned char *h
     for (int k = 0; k < KR; ++k) r[s][k] = (double)rsm[((size_t)s * Q + c * KR + k) * 32 + lane];
   }
   double pr[KR];
-  prior_from<Q, KR, MARKOV>(a, ti.item, c, lane, (const float *)pay + (size_t)DO_off * Q * 32, pr);
+  prior_from<Q, KR, MARKOV>(a, ti.item, c, lane, (const float *)xtra, pr);
   release_stage(empty, lane);
   vn_core<Q, KR, DV, MARKOV>(a, ti.fb, ti.item, qdst, r, pr, red, g, c, lane, frozen);
 }
@@ -1054,7 +1109,8 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
         for (int gg = 0; gg < G; ++gg)
           if (gg == g) s = su[gg];
         const bool done = sus_issue<Q, DMAX, MARKOV>(a, task, s, lvl_begin, ncols, sp.hdr + (size_t)k * kHdr,
-                                                     sp.pay + (size_t)k * Sh::PAYA, sp.bars + k);
+                                                     sp.pay + (size_t)k * Sh::PAYA,
+                                                     sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k);
 #pragma unroll
         for (int gg = 0; gg < G; ++gg)
           if (gg == g) su[gg] = s;
@@ -1065,10 +1121,10 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
   }
   const int cw = warp - 1, g = cw / T, c = cw % T;
   unsigned char *scr = sp.scr + (size_t)g * SS::SCR;
-  double *fwd = (double *)scr;
-  double *accs = fwd + SS::FWD_D;
-  double *red = accs + SS::ACC_D;
-  float *rsm = (float *)(red + SS::RED_D);
+  double *xp = (double *)scr;
+  double *red = (double *)scr;  // aliases the transpose buffers (used after them)
+  float *rsm = (float *)(scr + SS::XR_D * 8);
+  int m = 0;  // ping-pong transpose counter
   long long lo, hi;
   group_range(ntask, (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
   int rr = 0;  // units consumed by this group
@@ -1078,7 +1134,7 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
     for (int s = 0; s < nunits; ++s, ++rr) {
       const int st = rr % S, k = g * S + st;
       const unsigned char *hdr = sp.hdr + (size_t)k * kHdr;
-      const unsigned char *pay = sp.pay + (size_t)k * Sh::PAYA;
+      const unsigned char *xtra = sp.xtra + (size_t)k * Sh::XTRA_A;
       const uint32_t pay_u32 = sp.pay_u32 + (uint32_t)((size_t)k * Sh::PAYA);
       uint64_t *empty = sp.bars + G * S + k;
       mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
@@ -1088,47 +1144,51 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       const bool last = (s == nunits - 1);
       const bool frozen = a.early_exit && ((const int *)(hdr + 384))[lane] != 0;
       if (dv > 0) {
+#define SC(n) sus_check<Q, KR, n, DMAX>(a, hdr, pay_u32, empty, !last, xp, m, rsm, g, c, lane, frozen)
         switch (d - 1) {
-          case 0: sus_check<Q, KR, 0>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen); break;
-          case 1: sus_check<Q, KR, 1>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen); break;
-          case 2: sus_check<Q, KR, 2>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen); break;
+          case 0: SC(0); break;
+          case 1: SC(1); break;
+          case 2: SC(2); break;
           default:
             if constexpr (DO <= 3) {
-              sus_check<Q, KR, 3>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen);
+              SC(3);
             } else {
               switch (d - 1) {
-                case 3: sus_check<Q, KR, 3>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen); break;
-                case 4: sus_check<Q, KR, 4>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen); break;
-                case 5: sus_check<Q, KR, 5>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen); break;
-                case 6: sus_check<Q, KR, 6>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen); break;
-                default: sus_check<Q, KR, 7>(a, hdr, pay_u32, empty, !last, fwd, accs, rsm, g, c, lane, frozen); break;
+                case 3: SC(3); break;
+                case 4: SC(4); break;
+                case 5: SC(5); break;
+                case 6: SC(6); break;
+                default: SC(7); break;
               }
             }
             break;
         }
+#undef SC
       }
       if (last) {
         // vertical update of column j from the fresh r's (SUS step 2)
-        group_bar<T>(g);  // rsm complete
+        group_bar<T>(g);  // rsm complete, transpose buffers free for the reduction
+#define SV(n) sus_vn<Q, KR, n, DVMAX, MARKOV>(a, hdr, xtra, empty, rsm, red, g, c, lane, frozen)
         switch (dv) {
-          case 0: sus_vn<Q, KR, 0, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
-          case 1: sus_vn<Q, KR, 1, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
-          case 2: sus_vn<Q, KR, 2, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
+          case 0: SV(0); break;
+          case 1: SV(1); break;
+          case 2: SV(2); break;
           default:
             if constexpr (DVMAX <= 3) {
-              sus_vn<Q, KR, 3, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen);
+              SV(3);
             } else {
               switch (dv) {
-                case 3: sus_vn<Q, KR, 3, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
-                case 4: sus_vn<Q, KR, 4, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
-                case 5: sus_vn<Q, KR, 5, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
-                case 6: sus_vn<Q, KR, 6, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
-                case 7: sus_vn<Q, KR, 7, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
-                default: sus_vn<Q, KR, 8, DVMAX, MARKOV>(a, hdr, pay, DO, empty, rsm, red, g, c, lane, frozen); break;
+                case 3: SV(3); break;
+                case 4: SV(4); break;
+                case 5: SV(5); break;
+                case 6: SV(6); break;
+                case 7: SV(7); break;
+                default: SV(8); break;
               }
             }
             break;
         }
+#undef SV
       }
       group_bar<T>(g);  // transpose / reduction scratch and rsm free
     }
