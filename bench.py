@@ -214,14 +214,14 @@ def main():
     torch.cuda.set_device(local)
     import __graft_entry__
     __graft_entry__.build()
-    from paper_cs_0605069_b200 import gfq
+    from paper_cs_0605069_b200 import gfq, shard
 
     schedules = [gfq.GFQ_PUS if s == "pus" else gfq.GFQ_SUS for s in args.schedules.split(",")]
     code = synth.code_for(cfg)
     gcode = gfq.Code.from_synth(code)
     # rank r decodes frames [r*F, (r+1)*F) of the config's stream
     t_gen = time.perf_counter()
-    fr = synth.frames_for(cfg, code, range(rank * F, (rank + 1) * F), point=args.point)
+    fr = synth.frames_for(cfg, code, shard.frame_range(rank, world, F), point=args.point)
     t_gen = time.perf_counter() - t_gen
     ch = {synth.BSC: gfq.GFQ_BSC, synth.BEC: gfq.GFQ_BEC, synth.BIAWGN: gfq.GFQ_BIAWGN}[fr.channel]
     T = synth.markov_T_for(cfg)
@@ -262,9 +262,7 @@ def main():
     prof = gfq.gfq_profile_read()
     st = gfq.gfq_decode_stats(gcode, ws)
     if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = shard.max_over_ranks(ms, dist, device="cuda")   # the slowest rank's device time
         dist.barrier()
     bits_per_step_rank = len(schedules) * F * cfg.N * cfg.p
     value = bits_per_step_rank * world * args.steps / (ms / 1e3)
@@ -312,9 +310,7 @@ def main():
                 gfq.gfq_decode_host(gcode, obs_host, params[s], s_host, it_host, ws, stream)
         t_e2e = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t_e2e = float(t.item())
+            t_e2e = shard.max_over_ranks(t_e2e, dist, device="cuda")
         e2e = dict(value=bits_per_step_rank * world * args.steps / t_e2e, unit="bit/s",
                    h2d_bytes_per_step=int(obs_host.numel() * obs_host.element_size() * len(schedules)),
                    d2h_bytes_per_step=int((s_host.numel() + it_host.numel() * 4) * len(schedules)))

@@ -346,7 +346,7 @@ __device__ __forceinline__ void issue_extras(const WaveArgs &a, int fb, int j, u
 //      p(b) = [sum_a Q_{j-1}(a) T_ab] * [sum_c T_bc Q_{j+1}(c)]
 template <int Q, int KR, bool MARKOV>
 __device__ __forceinline__ void prior_from(const WaveArgs &a, int j, int c, int lane, const float *ex,
-                                           double (&pr)[KR]) {
+                                           const float *Tsm, double (&pr)[KR]) {
   using C = QC<Q, KR>;
   constexpr int P = C::P, LKR = C::LKR;
   const int N = a.c.N;
@@ -374,37 +374,40 @@ __device__ __forceinline__ void prior_from(const WaveArgs &a, int j, int c, int 
     for (int k = 0; k < KR; ++k) pr[k] = __ldg(a.pi0 + c * KR + k);
     return;
   }
-  double L[KR], R[KR];
+  // Eq. (7) factors accumulated in fp32 (all terms >= 0: no cancellation) from
+  // the fp32 snapshots, with T and T^T staged in shared memory (Ts): each
+  // thread reads its KR consecutive columns with 128-bit loads.
+  const float *Ts = Tsm;            // T[a][b]
+  const float *Tt = Tsm + Q * Q;    // T^T[c][b] = T[b][c]
+  float L[KR], R[KR];
   const float *exl = ex;           // rows of j-1 (issue_extras: slot 0)
   const float *exr = ex + Q * 32;  // rows of j+1 (slot 1)
-  if (j > 0) {
 #pragma unroll
-    for (int k = 0; k < KR; ++k) L[k] = 0.0;
+  for (int k = 0; k < KR; ++k) { L[k] = 0.0f; R[k] = 0.0f; }
+  if (j > 0) {
 #pragma unroll 4
     for (int x = 0; x < Q; ++x) {
-      const double qv = (double)exl[x * 32 + lane];
+      const float qv = exl[x * 32 + lane];
+      const float *trow = Ts + x * Q + c * KR;
 #pragma unroll
-      for (int k = 0; k < KR; ++k) L[k] += qv * __ldg(a.T + x * Q + c * KR + k);
+      for (int k = 0; k < KR; ++k) L[k] = fmaf(qv, trow[k], L[k]);
     }
-  } else {
-#pragma unroll
-    for (int k = 0; k < KR; ++k) L[k] = __ldg(a.pi0 + c * KR + k);
   }
   if (j < N - 1) {
-#pragma unroll
-    for (int k = 0; k < KR; ++k) R[k] = 0.0;
 #pragma unroll 4
     for (int x = 0; x < Q; ++x) {
-      const double qv = (double)exr[x * 32 + lane];
+      const float qv = exr[x * 32 + lane];
+      const float *trow = Tt + x * Q + c * KR;
 #pragma unroll
-      for (int k = 0; k < KR; ++k) R[k] += __ldg(a.T + (c * KR + k) * Q + x) * qv;
+      for (int k = 0; k < KR; ++k) R[k] = fmaf(qv, trow[k], R[k]);
     }
-  } else {
-#pragma unroll
-    for (int k = 0; k < KR; ++k) R[k] = 1.0;
   }
 #pragma unroll
-  for (int k = 0; k < KR; ++k) pr[k] = L[k] * R[k];
+  for (int k = 0; k < KR; ++k) {
+    const double l = (j > 0) ? (double)L[k] : __ldg(a.pi0 + c * KR + k);
+    const double r = (j < N - 1) ? (double)R[k] : 1.0;
+    pr[k] = l * r;
+  }
 }
 
 // ============================================================== variable node
@@ -594,21 +597,23 @@ struct PPof {
 // ============================================================== shared-memory layout
 // [mbarriers][G*S headers of kHdr][pad][G*S payload slots, each a multiple of
 // PAL = q*128 bytes and PAL-aligned in the shared window][G scratch areas]
-template <int Q, int S, int G, size_t PAY, size_t SCR, size_t XTRA = 0>
+template <int Q, int S, int G, size_t PAY, size_t SCR, size_t XTRA = 0, size_t TSMB = 0>
 struct Shape {
+  static constexpr size_t TSM_B = ((TSMB + 127) / 128) * 128;
   static constexpr size_t PAL = (size_t)Q * 128;
   static constexpr size_t PAYA = ((PAY + PAL - 1) / PAL) * PAL;
   static constexpr size_t BARS_B = ((16 * S * G + 127) / 128) * 128;
   static constexpr size_t HDR_B = (size_t)G * S * kHdr;
   static constexpr size_t XTRA_A = ((XTRA + 127) / 128) * 128;
   static constexpr size_t XTRA_B = (size_t)G * S * XTRA_A;
-  static constexpr size_t SMEM = BARS_B + HDR_B + XTRA_B + PAL + (size_t)G * S * PAYA + (size_t)G * SCR;
+  static constexpr size_t SMEM = BARS_B + HDR_B + XTRA_B + TSM_B + PAL + (size_t)G * S * PAYA + (size_t)G * SCR;
 };
 
 struct SmemPtrs {
   uint64_t *bars;
   unsigned char *hdr;
   unsigned char *xtra;
+  float *tsm;
   unsigned char *pay;
   uint32_t pay_u32;
   unsigned char *scr;
@@ -620,8 +625,9 @@ __device__ __forceinline__ SmemPtrs smem_ptrs(unsigned char *smem) {
   p.bars = (uint64_t *)smem;
   p.hdr = smem + Sh::BARS_B;
   p.xtra = p.hdr + Sh::HDR_B;
+  p.tsm = (float *)(p.xtra + Sh::XTRA_B);
   const uint32_t base = smem_u32(smem);
-  const uint32_t want = base + (uint32_t)(Sh::BARS_B + Sh::HDR_B + Sh::XTRA_B);
+  const uint32_t want = base + (uint32_t)(Sh::BARS_B + Sh::HDR_B + Sh::XTRA_B + Sh::TSM_B);
   const uint32_t al = (uint32_t)(((want + Sh::PAL - 1) / Sh::PAL) * Sh::PAL);
   p.pay = smem + (al - base);
   p.pay_u32 = al;
@@ -831,7 +837,7 @@ struct VNShape {
   static constexpr int XR = Extra<Q, MARKOV>::rows;
   static constexpr size_t PAY = (size_t)DVMAX * Q * 128;
   static constexpr size_t SCR = ((size_t)(DVMAX + 2) * T * 32 + (size_t)(DVMAX + 2) * 32 + T * 32) * 8;
-  using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128>;
+  using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, MARKOV ? (size_t)2 * Q * Q * 4 : 0>;
   static constexpr size_t SMEM = Sh::SMEM;
   static constexpr int THREADS = (1 + G * T) * 32;
 };
@@ -856,8 +862,8 @@ __device__ __forceinline__ void vn_issue(const WaveArgs &a, long long task, unsi
 
 template <int Q, int KR, int DV, int DVMAX, bool MARKOV>
 __device__ __forceinline__ void vn_task(const WaveArgs &a, const unsigned char *hdr, const unsigned char *pay,
-                                        const unsigned char *xtra, uint64_t *empty, double *red, int g, int c,
-                                        int lane) {
+                                        const unsigned char *xtra, const float *Tsm, uint64_t *empty, double *red,
+                                        int g, int c, int lane) {
   const TaskInfo ti = *(const TaskInfo *)hdr;
   const VarDesc *vd = (const VarDesc *)(hdr + 192);
   const bool frozen = a.early_exit && ((const int *)(hdr + 384))[lane] != 0;
@@ -871,7 +877,7 @@ __device__ __forceinline__ void vn_task(const WaveArgs &a, const unsigned char *
     for (int k = 0; k < KR; ++k) r[s][k] = (double)in[(s * Q + k) * 32];
   }
   double pr[KR];
-  prior_from<Q, KR, MARKOV>(a, ti.item, c, lane, (const float *)xtra, pr);
+  prior_from<Q, KR, MARKOV>(a, ti.item, c, lane, (const float *)xtra, Tsm, pr);
   release_stage(empty, lane);
   vn_core<Q, KR, DV, MARKOV>(a, ti.fb, ti.item, qdst, r, pr, red, g, c, lane, frozen);
 }
@@ -886,6 +892,10 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
   const SmemPtrs sp = smem_ptrs<Sh, S, G>(smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) init_bars<S, G>(sp.bars, T);
+  if constexpr (MARKOV) {
+    if (a.Tf)
+      for (int k = threadIdx.x; k < 2 * Q * Q; k += blockDim.x) sp.tsm[k] = a.Tf[k];
+  }
   __syncthreads();
   const int V = a.c.V;
   const long long ntask = (long long)(*a.nactive) * V;
@@ -912,20 +922,20 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
     mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
     const int dv = ((const TaskInfo *)hdr)->deg;
     switch (dv) {
-      case 0: vn_task<Q, KR, 0, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
-      case 1: vn_task<Q, KR, 1, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
-      case 2: vn_task<Q, KR, 2, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
+      case 0: vn_task<Q, KR, 0, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
+      case 1: vn_task<Q, KR, 1, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
+      case 2: vn_task<Q, KR, 2, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
       default:
         if constexpr (DVMAX <= 3) {
-          vn_task<Q, KR, 3, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane);
+          vn_task<Q, KR, 3, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane);
         } else {
           switch (dv) {
-            case 3: vn_task<Q, KR, 3, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
-            case 4: vn_task<Q, KR, 4, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
-            case 5: vn_task<Q, KR, 5, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
-            case 6: vn_task<Q, KR, 6, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
-            case 7: vn_task<Q, KR, 7, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
-            default: vn_task<Q, KR, 8, DVMAX, MARKOV>(a, hdr, pay, xtra, empty, red, g, c, lane); break;
+            case 3: vn_task<Q, KR, 3, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
+            case 4: vn_task<Q, KR, 4, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
+            case 5: vn_task<Q, KR, 5, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
+            case 6: vn_task<Q, KR, 6, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
+            case 7: vn_task<Q, KR, 7, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
+            default: vn_task<Q, KR, 8, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
           }
         }
         break;
@@ -948,7 +958,7 @@ struct SUSShape {
   static constexpr size_t XR_D = XP_D > RED_D ? XP_D : RED_D;
   static constexpr size_t RSM_F = (size_t)DVMAX * Q * 32;
   static constexpr size_t SCR = XR_D * 8 + RSM_F * 4;
-  using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128>;
+  using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, MARKOV ? (size_t)2 * Q * Q * 4 : 0>;
   static constexpr size_t SMEM = Sh::SMEM;
   static constexpr int THREADS = (1 + G * T) * 32;
 };
@@ -1061,8 +1071,8 @@ __device__ __forceinline__ void sus_check(const WaveArgs &a, const unsigned char
 
 template <int Q, int KR, int DV, int DVMAX, bool MARKOV>
 __device__ __forceinline__ void sus_vn(const WaveArgs &a, const unsigned char *hdr, const unsigned char *xtra,
-                                       uint64_t *empty, const float *rsm, double *red, int g, int c, int lane,
-                                       bool frozen) {
+                                       const float *Tsm, uint64_t *empty, const float *rsm, double *red, int g,
+                                       int c, int lane, bool frozen) {
   const TaskInfo ti = *(const TaskInfo *)hdr;
   const VarDesc *vd = (const VarDesc *)(hdr + 192);
   int qdst[DV > 0 ? DV : 1];
@@ -1074,7 +1084,7 @@ __device__ __forceinline__ void sus_vn(const WaveArgs &a, const unsigned char *h
     for (int k = 0; k < KR; ++k) r[s][k] = (double)rsm[((size_t)s * Q + c * KR + k) * 32 + lane];
   }
   double pr[KR];
-  prior_from<Q, KR, MARKOV>(a, ti.item, c, lane, (const float *)xtra, pr);
+  prior_from<Q, KR, MARKOV>(a, ti.item, c, lane, (const float *)xtra, Tsm, pr);
   release_stage(empty, lane);
   vn_core<Q, KR, DV, MARKOV>(a, ti.fb, ti.item, qdst, r, pr, red, g, c, lane, frozen);
 }
@@ -1095,6 +1105,10 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
   const SmemPtrs sp = smem_ptrs<Sh, S, G>(smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) init_bars<S, G>(sp.bars, T);
+  if constexpr (MARKOV) {
+    if (a.Tf)
+      for (int k = threadIdx.x; k < 2 * Q * Q; k += blockDim.x) sp.tsm[k] = a.Tf[k];
+  }
   __syncthreads();
   const long long ntask = (long long)(*a.nactive) * ncols;
   if (warp == 0) {
@@ -1168,7 +1182,7 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       if (last) {
         // vertical update of column j from the fresh r's (SUS step 2)
         group_bar<T>(g);  // rsm complete, transpose buffers free for the reduction
-#define SV(n) sus_vn<Q, KR, n, DVMAX, MARKOV>(a, hdr, xtra, empty, rsm, red, g, c, lane, frozen)
+#define SV(n) sus_vn<Q, KR, n, DVMAX, MARKOV>(a, hdr, xtra, sp.tsm, empty, rsm, red, g, c, lane, frozen)
         switch (dv) {
           case 0: SV(0); break;
           case 1: SV(1); break;

@@ -36,6 +36,7 @@ Layout make_layout(const gfq_code *c, int fbw, const gfq_params *prm) {
   L.stats = take(4 * sizeof(unsigned long long));
   L.nactive = take(sizeof(int));
   L.T = take((size_t)c->q * c->q * sizeof(double));
+  L.Tf = take((size_t)2 * c->q * c->q * sizeof(float));
   L.pi0 = take((size_t)c->q * sizeof(double));
   const size_t msg = (size_t)c->E * c->q * F32 * sizeof(float);
   L.qmsg = take(msg);
@@ -200,6 +201,15 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
   ce = cudaMemcpyAsync(at<double>(ws, L.T), hbuf.data(), sizeof(double) * q * q, cudaMemcpyHostToDevice, st);
   if (ce == cudaSuccess)
     ce = cudaMemcpyAsync(at<double>(ws, L.pi0), hbuf.data() + (size_t)q * q, sizeof(double) * q, cudaMemcpyHostToDevice, st);
+  std::vector<float> tf((size_t)2 * q * q, 0.0f);
+  if (prm->markov_T)
+    for (int x = 0; x < q; ++x)
+      for (int y = 0; y < q; ++y) {
+        tf[(size_t)x * q + y] = (float)prm->markov_T[x * q + y];              // T
+        tf[(size_t)q * q + (size_t)y * q + x] = (float)prm->markov_T[x * q + y];  // T^T
+      }
+  if (ce == cudaSuccess)
+    ce = cudaMemcpyAsync(at<float>(ws, L.Tf), tf.data(), sizeof(float) * 2 * q * q, cudaMemcpyHostToDevice, st);
   // (pageable H2D copies are staged before cudaMemcpyAsync returns, so hbuf may die here)
   if (ce == cudaSuccess) ce = cudaMemsetAsync(at<unsigned long long>(ws, L.stats), 0, 4 * sizeof(unsigned long long), st);
   if (ce != cudaSuccess) return cuda_fail(ce, "upload decoder constants");
@@ -246,6 +256,7 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
     a.nactive = at<int>(ws, L.nactive);
     a.stats = at<unsigned long long>(ws, L.stats);
     a.T = prm->markov_T ? at<double>(ws, L.T) : nullptr;
+    a.Tf = prm->markov_T ? at<float>(ws, L.Tf) : nullptr;
     a.pi0 = at<double>(ws, L.pi0);
     a.markov = prm->markov_T != nullptr;
     a.early_exit = prm->early_exit ? 1 : 0;

@@ -89,7 +89,7 @@ int cuda_fail(cudaError_t e, const char *what);
 struct Layout {
   int fbw;            // frame blocks per wave
   size_t qmsg, rmsg, pi, hard, z, xhat, qs0, qs1, qall, iters, conv, unsat, newconv;
-  size_t active, list, nactive, stats, T, pi0, total;
+  size_t active, list, nactive, stats, T, Tf, pi0, total;
 };
 Layout make_layout(const gfq_code *c, int fbw, const gfq_params *prm);
 
@@ -116,6 +116,7 @@ struct WaveArgs {
   int *nactive;         // [1]
   unsigned long long *stats;  // [4]
   const double *T;      // [q*q] or null
+  const float *Tf;      // [2*q*q] fp32 copies of T (row-major) and of T^T, or null
   const double *pi0;    // [q]
   int markov;
   int t;                // current iteration (1-based)

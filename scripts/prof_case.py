@@ -14,6 +14,8 @@ gc = gfq.Code.from_synth(code)
 ch = {synth.BSC: gfq.GFQ_BSC, synth.BEC: gfq.GFQ_BEC, synth.BIAWGN: gfq.GFQ_BIAWGN}[fr.channel]
 prm = gfq.Params(ch, fr.ch_param, sched, iters, early_exit=False, markov_T=synth.markov_T_for(cfg))
 obs = torch.as_tensor(fr.obs).cuda()
-s, it, ws = gfq.gfq_decode(gc, obs, prm)
+free, _ = torch.cuda.mem_get_info()
+ws = gfq.alloc_workspace(min(gfq.gfq_workspace_bytes(gc, nf, prm), free - (3 << 30)))
+s, it, ws = gfq.gfq_decode(gc, obs, prm, workspace=ws)
 torch.cuda.synchronize()
 print("ok", name, nf, sched, iters, gfq.gfq_decode_stats(gc, ws))
