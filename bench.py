@@ -282,18 +282,23 @@ def main():
     roof = None
     if alg_bytes is not None:
         achieved = alg_bytes / (dom_ms / 1e3) / 1e9
-        traffic = None
-        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tpath):
+        traffic, traffic_src = None, None
+        import glob
+        for tpath in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_traffic.json")), reverse=True):
             try:
                 tj = json.load(open(tpath))
-                if tj.get("config") == cfg.name and dom in tj.get("kernels", {}):
-                    traffic = tj["kernels"][dom]["dram_bytes_per_launch"]
             except Exception:
-                traffic = None
+                continue
+            kk = tj.get("kernels", {}).get(dom)
+            if tj.get("config") == cfg.name and kk and kk.get("dram_per_alg_byte"):
+                # ncu dram__bytes_read+write of one captured launch, as bytes per algorithmic
+                # byte, applied to this run's average launch
+                traffic = kk["dram_per_alg_byte"] * alg_bytes / dom_n
+                traffic_src = os.path.relpath(tpath, ROOT)
+                break
         roof = dict(bound="hbm", kernel=dom, achieved=achieved, peak=peak, unit="GB/s",
                     frac=achieved / peak, traffic=traffic,
-                    alg_bytes_per_launch=alg_bytes / dom_n, launches=dom_n,
+                    alg_bytes_per_launch=alg_bytes / dom_n, launches=dom_n, traffic_source=traffic_src,
                     avg_launch_ms=dom_ms / dom_n, peak_source=peak_src)
     # whole-step model bandwidth (all kernels)
     model_gbs = model_bytes_per_frame_iter(cfg) * F * iters * len(schedules) * args.steps / (ms / 1e3) / 1e9

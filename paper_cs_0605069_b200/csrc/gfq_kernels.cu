@@ -95,25 +95,26 @@ __global__ void k_init_msgs(WaveArgs a) {
   const int q = a.c.q, p = a.c.p, N = a.c.N;
   const long long E = a.c.E;
   const size_t Mp = (size_t)a.c.M * p;
-  const long long n = (long long)a.nfb * E * q * 32;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
-    const int lane = (int)(t & 31);
-    const int x = (int)((t >> 5) % q);
-    const long long r = (t >> 5) / q;
-    const int e = (int)(r % E);
-    const int fb = (int)(r / E);
+  const int lane = threadIdx.x & 31;
+  // one warp per (block, edge): lane = frame, loop over the q rows
+  const long long nw = (long long)a.nfb * E;
+  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nw;
+       w += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const int e = (int)(w % E);
+    const int fb = (int)(w / E);
     const int j = __ldg(a.c.edge_var + e);
-    double v;
+    float *dst = a.qmsg + (size_t)w * q * 32 + lane;
     if (j >= N) {
-      v = 1.0;
-      for (int b = 0; b < p; ++b) {
-        const double pb = (double)a.pi[((size_t)fb * Mp + (size_t)(j - N) * p + b) * 32 + lane];
-        v *= ((x >> b) & 1) ? pb : 1.0 - pb;
+      double pb[6];
+      for (int b = 0; b < p; ++b) pb[b] = (double)a.pi[((size_t)fb * Mp + (size_t)(j - N) * p + b) * 32 + lane];
+      for (int x = 0; x < q; ++x) {
+        double v = 1.0;
+        for (int b = 0; b < p; ++b) v *= ((x >> b) & 1) ? pb[b] : 1.0 - pb[b];
+        dst[x * 32] = (float)v;
       }
     } else {
-      v = __ldg(a.pi0 + x);
+      for (int x = 0; x < q; ++x) dst[x * 32] = (float)__ldg(a.pi0 + x);
     }
-    a.qmsg[t] = (float)v;
   }
 }
 
