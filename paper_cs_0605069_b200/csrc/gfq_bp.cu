@@ -83,9 +83,15 @@ constexpr int fit_stages(size_t per_stage, size_t other, int max_s) {
 #ifndef GFQ_G_T8
 #define GFQ_G_T8 2
 #endif
+// dedicated producer warp (small q: short tasks) vs one producer lane per
+// group (q = 64: keeps the CTA at 16 warps and 128 registers per thread)
+template <int T>
+struct PWof {
+  static constexpr bool v = (T == 2 || T == 4);  // measured: in-group producers win for T = 1 and 8
+};
 template <int T>
 struct Gof {
-  static constexpr int v = T >= 8 ? GFQ_G_T8 : (4 / T > 0 ? 4 / T : 1);
+  static constexpr int v = T >= 8 ? GFQ_G_T8 : (T >= 2 ? 2 : 4);
 };
 
 // ============================================================== PTX: mbarrier + TMA bulk copy
@@ -690,7 +696,7 @@ struct CNShape {
   static constexpr size_t SCR = T > 1 ? (size_t)(PP ? 2 : DMAX) * Q * 32 * 8 : 0;
   using Sh = Shape<Q, S, G, PAY, SCR>;
   static constexpr size_t SMEM = Sh::SMEM;
-  static constexpr int THREADS = (1 + G * T) * 32;
+  static constexpr int THREADS = (G * T + (PWof<T>::v ? 1 : 0)) * 32;
 };
 
 template <int Q, int DMAX>
@@ -718,9 +724,9 @@ __device__ __forceinline__ void cn_issue(const WaveArgs &a, long long task, unsi
 // reading A4).  The stored r is q * r (the 1/q of the inverse transform is
 // dropped: the variable node normalises, the export divides); negative
 // round-off is clamped to 0 (reading A20).
-template <int Q, int KR, int D, int DMAX>
+template <int Q, int KR, int D, int DMAX, typename RF>
 __device__ __forceinline__ void cn_task(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_u32,
-                                        uint64_t *empty, double *xp, int &m, int g, int c, int lane) {
+                                        uint64_t *empty, double *xp, int &m, int g, int c, int lane, RF &&refill) {
   using C = QC<Q, KR>;
   constexpr int T = C::T, LKR = C::LKR, LT = C::LT, P = C::P;
   constexpr bool PP = PPof<Q>::v;
@@ -744,6 +750,7 @@ __device__ __forceinline__ void cn_task(const WaveArgs &a, const unsigned char *
     for (int k = 0; k < KR; ++k) u[s][k] = (double)lds_f32(ad[k]);
   }
   release_stage(empty, lane);
+  refill();
 #pragma unroll
   for (int s = 0; s < D; ++s) wht_bits<KR, 0, LKR>(u[s]);
   if constexpr (T > 1) {
@@ -788,7 +795,8 @@ __global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(Wave
   __syncthreads();
   const int M = a.c.M;
   const long long ntask = (long long)(*a.nactive) * M;
-  if (warp == 0) {
+  constexpr bool PW = PWof<T>::v;
+  if (PW && warp == 0) {
     if (lane == 0)
       produce<S, G>(sp.bars, ntask, [&](int g, int st, long long task) {
         const int k = g * S + st;
@@ -797,33 +805,49 @@ __global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(Wave
       });
     return;
   }
-  const int cw = warp - 1, g = cw / T, c = cw % T;
+  const int cw = PW ? warp - 1 : warp;
+  const int g = cw / T, c = cw % T;
+  const bool producer = !PW && (c == 0) && (lane == 0);  // one lane per group issues its TMA copies
   double *xp = (double *)(sp.scr + (size_t)g * CS::SCR);
   int m = 0;  // ping-pong transpose counter
   long long lo, hi;
   group_range(ntask, (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
+  if (producer)
+    for (int n = 0; n < S && lo + n < hi; ++n) {
+      const int k = g * S + n;
+      cn_issue<Q, DMAX>(a, lo + n, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA, sp.bars + k);
+    }
   for (long long task = lo; task < hi; ++task) {
     const int rr = (int)(task - lo), st = rr % S, k = g * S + st;
-    const unsigned char *hdr = sp.hdr + (size_t)k * kHdr;
+    unsigned char *hdrw = sp.hdr + (size_t)k * kHdr;
+    const unsigned char *hdr = hdrw;
     const uint32_t pay = sp.pay_u32 + (uint32_t)((size_t)k * Sh::PAYA);
     uint64_t *empty = sp.bars + G * S + k;
+    // refill stage k with task + S once every warp of the group has released it
+    auto refill = [&]() {
+      if (producer && task + S < hi) {
+        mbar_wait(empty, (uint32_t)((rr / S) & 1));
+        cn_issue<Q, DMAX>(a, task + S, hdrw, sp.pay + (size_t)k * Sh::PAYA, sp.bars + k);
+      }
+    };
     mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
     const int d = ((const TaskInfo *)hdr)->deg;
     switch (d) {
-      case 1: cn_task<Q, KR, 1, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane); break;
-      case 2: cn_task<Q, KR, 2, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane); break;
-      case 3: cn_task<Q, KR, 3, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane); break;
-      case 4: cn_task<Q, KR, 4, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane); break;
+      case 1: cn_task<Q, KR, 1, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane, refill); break;
+      case 2: cn_task<Q, KR, 2, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane, refill); break;
+      case 3: cn_task<Q, KR, 3, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane, refill); break;
+      case 4: cn_task<Q, KR, 4, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane, refill); break;
       default:
         if constexpr (DMAX > 4) {
           switch (d) {
-            case 5: cn_task<Q, KR, 5, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane); break;
-            case 6: cn_task<Q, KR, 6, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane); break;
-            case 7: cn_task<Q, KR, 7, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane); break;
-            default: cn_task<Q, KR, 8, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane); break;
+            case 5: cn_task<Q, KR, 5, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane, refill); break;
+            case 6: cn_task<Q, KR, 6, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane, refill); break;
+            case 7: cn_task<Q, KR, 7, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane, refill); break;
+            default: cn_task<Q, KR, 8, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane, refill); break;
           }
         } else {
           release_stage(empty, lane);  // d == 0: an empty check has no edge
+          refill();
         }
         break;
     }
@@ -839,7 +863,7 @@ struct VNShape {
   static constexpr size_t SCR = ((size_t)(DVMAX + 2) * T * 32 + (size_t)(DVMAX + 2) * 32 + T * 32) * 8;
   using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, MARKOV ? (size_t)2 * Q * Q * 4 : 0>;
   static constexpr size_t SMEM = Sh::SMEM;
-  static constexpr int THREADS = (1 + G * T) * 32;
+  static constexpr int THREADS = (G * T + (PWof<T>::v ? 1 : 0)) * 32;
 };
 
 template <int Q, int DVMAX, bool MARKOV>
@@ -860,10 +884,10 @@ __device__ __forceinline__ void vn_issue(const WaveArgs &a, long long task, unsi
   issue_extras<Q, MARKOV>(a, fb, j, xtra, full);
 }
 
-template <int Q, int KR, int DV, int DVMAX, bool MARKOV>
+template <int Q, int KR, int DV, int DVMAX, bool MARKOV, typename RF>
 __device__ __forceinline__ void vn_task(const WaveArgs &a, const unsigned char *hdr, const unsigned char *pay,
                                         const unsigned char *xtra, const float *Tsm, uint64_t *empty, double *red,
-                                        int g, int c, int lane) {
+                                        int g, int c, int lane, RF &&refill) {
   const TaskInfo ti = *(const TaskInfo *)hdr;
   const VarDesc *vd = (const VarDesc *)(hdr + 192);
   const bool frozen = a.early_exit && ((const int *)(hdr + 384))[lane] != 0;
@@ -879,6 +903,7 @@ __device__ __forceinline__ void vn_task(const WaveArgs &a, const unsigned char *
   double pr[KR];
   prior_from<Q, KR, MARKOV>(a, ti.item, c, lane, (const float *)xtra, Tsm, pr);
   release_stage(empty, lane);
+  refill();
   vn_core<Q, KR, DV, MARKOV>(a, ti.fb, ti.item, qdst, r, pr, red, g, c, lane, frozen);
 }
 
@@ -899,7 +924,8 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
   __syncthreads();
   const int V = a.c.V;
   const long long ntask = (long long)(*a.nactive) * V;
-  if (warp == 0) {
+  constexpr bool PW = PWof<T>::v;
+  if (PW && warp == 0) {
     if (lane == 0)
       produce<S, G>(sp.bars, ntask, [&](int g, int st, long long task) {
         const int k = g * S + st;
@@ -909,37 +935,55 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
       });
     return;
   }
-  const int cw = warp - 1, g = cw / T, c = cw % T;
+  const int cw = PW ? warp - 1 : warp;
+  const int g = cw / T, c = cw % T;
+  const bool producer = !PW && (c == 0) && (lane == 0);
   double *red = (double *)(sp.scr + (size_t)g * VS::SCR);
   long long lo, hi;
   group_range(ntask, (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
+  if (producer)
+    for (int n = 0; n < S && lo + n < hi; ++n) {
+      const int k = g * S + n;
+      vn_issue<Q, DVMAX, MARKOV>(a, lo + n, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA,
+                                 sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k, clip_only);
+    }
   for (long long task = lo; task < hi; ++task) {
     const int rr = (int)(task - lo), st = rr % S, k = g * S + st;
-    const unsigned char *hdr = sp.hdr + (size_t)k * kHdr;
+    unsigned char *hdrw = sp.hdr + (size_t)k * kHdr;
+    const unsigned char *hdr = hdrw;
     const unsigned char *pay = sp.pay + (size_t)k * Sh::PAYA;
     const unsigned char *xtra = sp.xtra + (size_t)k * Sh::XTRA_A;
     uint64_t *empty = sp.bars + G * S + k;
+    auto refill = [&]() {
+      if (producer && task + S < hi) {
+        mbar_wait(empty, (uint32_t)((rr / S) & 1));
+        vn_issue<Q, DVMAX, MARKOV>(a, task + S, hdrw, sp.pay + (size_t)k * Sh::PAYA, sp.xtra + (size_t)k * Sh::XTRA_A,
+                                   sp.bars + k, clip_only);
+      }
+    };
     mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
     const int dv = ((const TaskInfo *)hdr)->deg;
+#define VT(n) vn_task<Q, KR, n, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane, refill)
     switch (dv) {
-      case 0: vn_task<Q, KR, 0, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
-      case 1: vn_task<Q, KR, 1, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
-      case 2: vn_task<Q, KR, 2, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
+      case 0: VT(0); break;
+      case 1: VT(1); break;
+      case 2: VT(2); break;
       default:
         if constexpr (DVMAX <= 3) {
-          vn_task<Q, KR, 3, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane);
+          VT(3);
         } else {
           switch (dv) {
-            case 3: vn_task<Q, KR, 3, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
-            case 4: vn_task<Q, KR, 4, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
-            case 5: vn_task<Q, KR, 5, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
-            case 6: vn_task<Q, KR, 6, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
-            case 7: vn_task<Q, KR, 7, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
-            default: vn_task<Q, KR, 8, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane); break;
+            case 3: VT(3); break;
+            case 4: VT(4); break;
+            case 5: VT(5); break;
+            case 6: VT(6); break;
+            case 7: VT(7); break;
+            default: VT(8); break;
           }
         }
         break;
     }
+#undef VT
     if constexpr (T > 1) group_bar<T>(g);  // red reusable
   }
 }
@@ -960,7 +1004,7 @@ struct SUSShape {
   static constexpr size_t SCR = XR_D * 8 + RSM_F * 4;
   using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, MARKOV ? (size_t)2 * Q * Q * 4 : 0>;
   static constexpr size_t SMEM = Sh::SMEM;
-  static constexpr int THREADS = (1 + G * T) * 32;
+  static constexpr int THREADS = (G * T + (PWof<T>::v ? 1 : 0)) * 32;
 };
 
 // Units: one per (column, check slot) -- the check's other edges in at most
@@ -1007,10 +1051,10 @@ __device__ __forceinline__ bool sus_issue(const WaveArgs &a, long long task, int
 // Step 1 of SUS for one check (exact number of other edges DO): r_ij from the
 // CURRENT q's of the check's other edges (the transform of k_cn restricted to
 // one output).  Writes q * r_ij into rsm slot s in natural order a.
-template <int Q, int KR, int DO, int DMAX>
+template <int Q, int KR, int DO, int DMAX, typename RF>
 __device__ __forceinline__ void sus_check(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_u32,
                                           uint64_t *empty, bool release, double *xp, int &m, float *rsm, int g,
-                                          int c, int lane, bool frozen) {
+                                          int c, int lane, bool frozen, RF &&refill) {
   using C = QC<Q, KR>;
   constexpr int T = C::T, LKR = C::LKR, LT = C::LT, P = C::P;
   constexpr bool PP = PPof<Q>::v;
@@ -1027,7 +1071,10 @@ __device__ __forceinline__ void sus_check(const WaveArgs &a, const unsigned char
     for (int k = 0; k < KR; ++k) v[t][k] = (double)lds_f32(ad[k]);
   }
   const unsigned long long pke = sd->perm_e;
-  if (release) release_stage(empty, lane);
+  if (release) {
+    release_stage(empty, lane);
+    refill();
+  }
 #pragma unroll
   for (int t = 0; t < DO; ++t) wht_bits<KR, 0, LKR>(v[t]);
   if constexpr (T > 1) {
@@ -1069,10 +1116,10 @@ __device__ __forceinline__ void sus_check(const WaveArgs &a, const unsigned char
   }
 }
 
-template <int Q, int KR, int DV, int DVMAX, bool MARKOV>
+template <int Q, int KR, int DV, int DVMAX, bool MARKOV, typename RF>
 __device__ __forceinline__ void sus_vn(const WaveArgs &a, const unsigned char *hdr, const unsigned char *xtra,
                                        const float *Tsm, uint64_t *empty, const float *rsm, double *red, int g,
-                                       int c, int lane, bool frozen) {
+                                       int c, int lane, bool frozen, RF &&refill) {
   const TaskInfo ti = *(const TaskInfo *)hdr;
   const VarDesc *vd = (const VarDesc *)(hdr + 192);
   int qdst[DV > 0 ? DV : 1];
@@ -1086,6 +1133,7 @@ __device__ __forceinline__ void sus_vn(const WaveArgs &a, const unsigned char *h
   double pr[KR];
   prior_from<Q, KR, MARKOV>(a, ti.item, c, lane, (const float *)xtra, Tsm, pr);
   release_stage(empty, lane);
+  refill();
   vn_core<Q, KR, DV, MARKOV>(a, ti.fb, ti.item, qdst, r, pr, red, g, c, lane, frozen);
 }
 
@@ -1111,7 +1159,8 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
   }
   __syncthreads();
   const long long ntask = (long long)(*a.nactive) * ncols;
-  if (warp == 0) {
+  constexpr bool PW = PWof<T>::v;
+  if (PW && warp == 0) {
     if (lane == 0) {
       int su[G];
 #pragma unroll
@@ -1133,7 +1182,9 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
     }
     return;
   }
-  const int cw = warp - 1, g = cw / T, c = cw % T;
+  const int cw = PW ? warp - 1 : warp;
+  const int g = cw / T, c = cw % T;
+  const bool producer = !PW && (c == 0) && (lane == 0);
   unsigned char *scr = sp.scr + (size_t)g * SS::SCR;
   double *xp = (double *)scr;
   double *red = (double *)scr;  // aliases the transpose buffers (used after them)
@@ -1141,6 +1192,18 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
   int m = 0;  // ping-pong transpose counter
   long long lo, hi;
   group_range(ntask, (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
+  // producer cursor over (task, unit) of this group
+  long long ptask = lo;
+  int pu = 0, pissued = 0;
+  auto issue_next = [&](int k) {
+    if (ptask >= hi) return;
+    if (sus_issue<Q, DMAX, MARKOV>(a, ptask, pu, lvl_begin, ncols, sp.hdr + (size_t)k * kHdr,
+                                   sp.pay + (size_t)k * Sh::PAYA, sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k))
+      ++ptask;
+    ++pissued;
+  };
+  if (producer)
+    for (int n = 0; n < S; ++n) issue_next(g * S + n);
   int rr = 0;  // units consumed by this group
   for (long long task = lo; task < hi; ++task) {
     int nunits = 1;
@@ -1151,6 +1214,12 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       const unsigned char *xtra = sp.xtra + (size_t)k * Sh::XTRA_A;
       const uint32_t pay_u32 = sp.pay_u32 + (uint32_t)((size_t)k * Sh::PAYA);
       uint64_t *empty = sp.bars + G * S + k;
+      auto refill = [&]() {
+        if (producer && ptask < hi) {
+          mbar_wait(empty, (uint32_t)((rr / S) & 1));
+          issue_next(k);
+        }
+      };
       mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
       const TaskInfo *ti = (const TaskInfo *)hdr;
       const int dv = ti->deg, d = ti->d;
@@ -1158,7 +1227,7 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       const bool last = (s == nunits - 1);
       const bool frozen = a.early_exit && ((const int *)(hdr + 384))[lane] != 0;
       if (dv > 0) {
-#define SC(n) sus_check<Q, KR, n, DMAX>(a, hdr, pay_u32, empty, !last, xp, m, rsm, g, c, lane, frozen)
+#define SC(n) sus_check<Q, KR, n, DMAX>(a, hdr, pay_u32, empty, !last, xp, m, rsm, g, c, lane, frozen, refill)
         switch (d - 1) {
           case 0: SC(0); break;
           case 1: SC(1); break;
@@ -1182,7 +1251,7 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       if (last) {
         // vertical update of column j from the fresh r's (SUS step 2)
         group_bar<T>(g);  // rsm complete, transpose buffers free for the reduction
-#define SV(n) sus_vn<Q, KR, n, DVMAX, MARKOV>(a, hdr, xtra, sp.tsm, empty, rsm, red, g, c, lane, frozen)
+#define SV(n) sus_vn<Q, KR, n, DVMAX, MARKOV>(a, hdr, xtra, sp.tsm, empty, rsm, red, g, c, lane, frozen, refill)
         switch (dv) {
           case 0: SV(0); break;
           case 1: SV(1); break;
@@ -1207,6 +1276,7 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       group_bar<T>(g);  // transpose / reduction scratch and rsm free
     }
   }
+  (void)pissued;
 }
 
 // ============================================================== launchers

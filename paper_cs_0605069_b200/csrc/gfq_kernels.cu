@@ -297,7 +297,9 @@ int launch_init_state(const WaveArgs &a, cudaStream_t s) {
 }
 
 int launch_test(const WaveArgs &a, cudaStream_t s) {
-  const int chunk = 64;
+  // chunks of checks per warp task: enough tasks to give every SM 32 warps
+  const long long work = (long long)a.nfb * a.c.M;
+  const int chunk = (int)std::max<long long>(1, std::min<long long>(64, work / ((long long)sm_count() * 32)));
   const int threads = 256;
   const long long tasks = (long long)a.nfb * ((a.c.M + chunk - 1) / chunk);
   const int grid = (int)std::max<long long>(1, std::min<long long>((tasks + 7) / 8, (long long)sm_count() * 8));
