@@ -66,10 +66,14 @@ struct QC {
 #define GFQ_KR_SUS16 8
 #endif
 enum KernelKind { KCN, KVN, KSUS };
+#ifndef GFQ_KR64
+#define GFQ_KR64 8
+#endif
 template <int Q, int K>
 struct KRof {
   static constexpr int v = Q <= 8 ? Q
                            : Q == 16 ? (K == KCN ? GFQ_KR_CN16 : K == KVN ? GFQ_KR_VN16 : GFQ_KR_SUS16)
+                           : Q == 64 ? GFQ_KR64
                                      : 8;
 };
 // largest stage count in [2, max_s] such that the CTA fits the 227 KB of
@@ -80,18 +84,28 @@ constexpr int fit_stages(size_t per_stage, size_t other, int max_s) {
 }
 
 // groups per CTA for a given number of warps per group
-#ifndef GFQ_G_T8
-#define GFQ_G_T8 2
-#endif
 // dedicated producer warp (small q: short tasks) vs one producer lane per
 // group (q = 64: keeps the CTA at 16 warps and 128 registers per thread)
+#ifndef GFQ_PW_T4
+#define GFQ_PW_T4 1
+#endif
 template <int T>
 struct PWof {
-  static constexpr bool v = (T == 2 || T == 4);  // measured: in-group producers win for T = 1 and 8
+  static constexpr bool v = (T == 2 || (T == 4 && GFQ_PW_T4));  // measured: in-group producers win for T = 1, 8
 };
-template <int T>
+#ifndef GFQ_G_T8_CN
+#define GFQ_G_T8_CN 2
+#endif
+#ifndef GFQ_G_T8_VN
+#define GFQ_G_T8_VN 2
+#endif
+#ifndef GFQ_G_T8_SUS
+#define GFQ_G_T8_SUS 2
+#endif
+template <int T, int K = 0>
 struct Gof {
-  static constexpr int v = T >= 8 ? GFQ_G_T8 : (T >= 2 ? 2 : 4);
+  static constexpr int g8 = K == KCN ? GFQ_G_T8_CN : K == KVN ? GFQ_G_T8_VN : GFQ_G_T8_SUS;
+  static constexpr int v = T >= 8 ? g8 : (T >= 2 ? 2 : 4);
 };
 
 // ============================================================== PTX: mbarrier + TMA bulk copy
@@ -181,6 +195,18 @@ __device__ __forceinline__ int row_lo(const int (&bb)[P], int k) {  // image of 
 
 __device__ __forceinline__ double neg_if(double v, int s) {
   return __longlong_as_double(__double_as_longlong(v) ^ ((long long)s << 63));
+}
+
+// 1/x for a positive normal double: hardware approximation (rcp.approx.ftz.f64)
+// refined by two Newton steps (relative error far below the fp32 storage of
+// the normalised message).
+__device__ __forceinline__ double fast_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
 }
 
 // Flip the sign of a double by XOR-ing its high word with a 0 / 0x80000000 mask.
@@ -519,7 +545,7 @@ __device__ __forceinline__ void vn_core(const WaveArgs &a, int fb, int j, const 
     const double sm = sums[s];
     const bool ok = sm > 0.0 && isfinite(sm);
     bad += !ok;
-    const double inv = ok ? 1.0 / sm : 0.0;
+    const double inv = ok ? fast_rcp(sm) : 0.0;
     const float add = ok ? 0.0f : 1.0f / Q;
     if (!frozen) {
       float *dst = a.qmsg + ((size_t)fb * E + qdst[s]) * Q * 32 + lane + c * KR * 32;
@@ -531,7 +557,7 @@ __device__ __forceinline__ void vn_core(const WaveArgs &a, int fb, int j, const 
   const bool okq = st > 0.0 && isfinite(st);
   bad += !okq;
   if (!okq) bidx = 0;
-  const double invq = okq ? 1.0 / st : 0.0;
+  const double invq = okq ? fast_rcp(st) : 0.0;
   const float addq = okq ? 0.0f : 1.0f / Q;
   if (!frozen) {
     if (MARKOV && j < a.c.N && a.qs_new) {
@@ -651,16 +677,48 @@ __device__ __forceinline__ void init_bars(uint64_t *bars, int T) {
   fence_mbar_init();
 }
 
-// Producer: lane 0 of warp 0 walks every consumer group's contiguous share of
-// tasks round-robin, refilling a stage as soon as its "empty" barrier flips.
+// Walk over a contiguous range of tasks (frame block, item) without 64-bit
+// divisions per task: the block index and item advance incrementally.
+struct Cursor {
+  long long t, hi;
+  int fbi, item, fb, nitems;
+  __device__ __forceinline__ void init(const WaveArgs &a, long long t0, long long hi_, int nitems_) {
+    t = t0;
+    hi = hi_;
+    nitems = nitems_;
+    fbi = item = fb = 0;
+    if (t < hi) {
+      fbi = (int)(t / nitems);
+      item = (int)(t - (long long)fbi * nitems);
+      fb = a.list[fbi];
+    }
+  }
+  __device__ __forceinline__ bool valid() const { return t < hi; }
+  __device__ __forceinline__ void advance(const WaveArgs &a) {
+    ++t;
+    if (++item == nitems) {
+      item = 0;
+      ++fbi;
+      if (t < hi) fb = a.list[fbi];
+    }
+  }
+};
+
+// Dedicated producer (lane 0 of warp 0): walks every consumer group's
+// contiguous share of tasks round-robin, refilling a stage as soon as its
+// "empty" barrier flips.  issue(g, st, cursor) returns true when the task is
+// complete (SUS tasks span several stages).
 template <int S, int G, typename Issue>
-__device__ __forceinline__ void produce(uint64_t *bars, long long ntask, Issue issue) {
+__device__ __forceinline__ void produce(const WaveArgs &a, uint64_t *bars, long long ntask, int nitems,
+                                        Issue issue) {
   const long long ngroups = (long long)gridDim.x * G;
-  long long t[G], hi[G];
+  Cursor cur[G];
   int ring[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    group_range(ntask, (long long)blockIdx.x * G + g, ngroups, t[g], hi[g]);
+    long long lo, hi;
+    group_range(ntask, (long long)blockIdx.x * G + g, ngroups, lo, hi);
+    cur[g].init(a, lo, hi, nitems);
     ring[g] = 0;
   }
   for (bool any = true; any;) {
@@ -668,7 +726,7 @@ __device__ __forceinline__ void produce(uint64_t *bars, long long ntask, Issue i
     bool did = false;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      if (t[g] >= hi[g]) continue;
+      if (!cur[g].valid()) continue;
       any = true;
       const int st = ring[g] % S, u = ring[g] / S;
       if (u > 0) {
@@ -679,7 +737,7 @@ __device__ __forceinline__ void produce(uint64_t *bars, long long ntask, Issue i
           continue;
         }
       }
-      if (issue(g, st, t[g])) ++t[g];
+      if (issue(g, st, cur[g])) cur[g].advance(a);
       ++ring[g];
       did = true;
     }
@@ -700,11 +758,9 @@ struct CNShape {
 };
 
 template <int Q, int DMAX>
-__device__ __forceinline__ void cn_issue(const WaveArgs &a, long long task, unsigned char *hdr, unsigned char *pay,
+__device__ __forceinline__ void cn_issue(const WaveArgs &a, int fb, int i, unsigned char *hdr, unsigned char *pay,
                                          uint64_t *full) {
   const int M = a.c.M;
-  const int fb = a.list[task / M];
-  const int i = (int)(task % M);
   const int e0 = __ldg(a.c.row_ptr + i), d = __ldg(a.c.row_ptr + i + 1) - e0;
   TaskInfo *ti = (TaskInfo *)hdr;
   ti->fb = fb; ti->item = i; ti->e0 = e0; ti->deg = d;
@@ -798,9 +854,9 @@ __global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(Wave
   constexpr bool PW = PWof<T>::v;
   if (PW && warp == 0) {
     if (lane == 0)
-      produce<S, G>(sp.bars, ntask, [&](int g, int st, long long task) {
+      produce<S, G>(a, sp.bars, ntask, M, [&](int g, int st, const Cursor &cu) {
         const int k = g * S + st;
-        cn_issue<Q, DMAX>(a, task, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA, sp.bars + k);
+        cn_issue<Q, DMAX>(a, cu.fb, cu.item, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA, sp.bars + k);
         return true;
       });
     return;
@@ -812,11 +868,14 @@ __global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(Wave
   int m = 0;  // ping-pong transpose counter
   long long lo, hi;
   group_range(ntask, (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
-  if (producer)
-    for (int n = 0; n < S && lo + n < hi; ++n) {
+  Cursor pc;
+  if (producer) {
+    pc.init(a, lo, hi, M);
+    for (int n = 0; n < S && pc.valid(); ++n, pc.advance(a)) {
       const int k = g * S + n;
-      cn_issue<Q, DMAX>(a, lo + n, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA, sp.bars + k);
+      cn_issue<Q, DMAX>(a, pc.fb, pc.item, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA, sp.bars + k);
     }
+  }
   for (long long task = lo; task < hi; ++task) {
     const int rr = (int)(task - lo), st = rr % S, k = g * S + st;
     unsigned char *hdrw = sp.hdr + (size_t)k * kHdr;
@@ -825,9 +884,10 @@ __global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(Wave
     uint64_t *empty = sp.bars + G * S + k;
     // refill stage k with task + S once every warp of the group has released it
     auto refill = [&]() {
-      if (producer && task + S < hi) {
+      if (producer && pc.valid()) {
         mbar_wait(empty, (uint32_t)((rr / S) & 1));
-        cn_issue<Q, DMAX>(a, task + S, hdrw, sp.pay + (size_t)k * Sh::PAYA, sp.bars + k);
+        cn_issue<Q, DMAX>(a, pc.fb, pc.item, hdrw, sp.pay + (size_t)k * Sh::PAYA, sp.bars + k);
+        pc.advance(a);
       }
     };
     mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
@@ -867,11 +927,8 @@ struct VNShape {
 };
 
 template <int Q, int DVMAX, bool MARKOV>
-__device__ __forceinline__ void vn_issue(const WaveArgs &a, long long task, unsigned char *hdr, unsigned char *pay,
+__device__ __forceinline__ void vn_issue(const WaveArgs &a, int fb, int j, unsigned char *hdr, unsigned char *pay,
                                          unsigned char *xtra, uint64_t *full, int clip_only) {
-  const int V = a.c.V;
-  const int fb = a.list[task / V];
-  const int j = (int)(task % V);
   const int e0 = __ldg(a.c.col_ptr + j);
   const int dv = clip_only ? 0 : __ldg(a.c.col_ptr + j + 1) - e0;
   TaskInfo *ti = (TaskInfo *)hdr;
@@ -927,9 +984,9 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
   constexpr bool PW = PWof<T>::v;
   if (PW && warp == 0) {
     if (lane == 0)
-      produce<S, G>(sp.bars, ntask, [&](int g, int st, long long task) {
+      produce<S, G>(a, sp.bars, ntask, V, [&](int g, int st, const Cursor &cu) {
         const int k = g * S + st;
-        vn_issue<Q, DVMAX, MARKOV>(a, task, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA,
+        vn_issue<Q, DVMAX, MARKOV>(a, cu.fb, cu.item, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA,
                                    sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k, clip_only);
         return true;
       });
@@ -941,12 +998,15 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
   double *red = (double *)(sp.scr + (size_t)g * VS::SCR);
   long long lo, hi;
   group_range(ntask, (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
-  if (producer)
-    for (int n = 0; n < S && lo + n < hi; ++n) {
+  Cursor pc;
+  if (producer) {
+    pc.init(a, lo, hi, V);
+    for (int n = 0; n < S && pc.valid(); ++n, pc.advance(a)) {
       const int k = g * S + n;
-      vn_issue<Q, DVMAX, MARKOV>(a, lo + n, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA,
+      vn_issue<Q, DVMAX, MARKOV>(a, pc.fb, pc.item, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA,
                                  sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k, clip_only);
     }
+  }
   for (long long task = lo; task < hi; ++task) {
     const int rr = (int)(task - lo), st = rr % S, k = g * S + st;
     unsigned char *hdrw = sp.hdr + (size_t)k * kHdr;
@@ -955,10 +1015,11 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
     const unsigned char *xtra = sp.xtra + (size_t)k * Sh::XTRA_A;
     uint64_t *empty = sp.bars + G * S + k;
     auto refill = [&]() {
-      if (producer && task + S < hi) {
+      if (producer && pc.valid()) {
         mbar_wait(empty, (uint32_t)((rr / S) & 1));
-        vn_issue<Q, DVMAX, MARKOV>(a, task + S, hdrw, sp.pay + (size_t)k * Sh::PAYA, sp.xtra + (size_t)k * Sh::XTRA_A,
-                                   sp.bars + k, clip_only);
+        vn_issue<Q, DVMAX, MARKOV>(a, pc.fb, pc.item, hdrw, sp.pay + (size_t)k * Sh::PAYA,
+                                   sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k, clip_only);
+        pc.advance(a);
       }
     };
     mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
@@ -1011,11 +1072,10 @@ struct SUSShape {
 // two contiguous runs; the last unit of a column also carries the prior's
 // extra rows and the column's VarDesc.
 template <int Q, int DMAX, bool MARKOV>
-__device__ __forceinline__ bool sus_issue(const WaveArgs &a, long long task, int &s, int lvl_begin, int ncols,
+__device__ __forceinline__ bool sus_issue(const WaveArgs &a, int fb, int col, int &s, int lvl_begin,
                                           unsigned char *hdr, unsigned char *pay, unsigned char *xtra,
                                           uint64_t *full) {
-  const int fb = a.list[task / ncols];
-  const LvlCol lc = a.c.lvl_col[lvl_begin + (int)(task % ncols)];
+  const LvlCol lc = a.c.lvl_col[lvl_begin + col];
   const int nunits = lc.dv > 0 ? lc.dv : 1;
   const LvlUnit un = a.c.lvl_unit[lc.unit0 + s];
   TaskInfo *ti = (TaskInfo *)hdr;
@@ -1165,13 +1225,13 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       int su[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) su[g] = 0;
-      produce<S, G>(sp.bars, ntask, [&](int g, int st, long long task) {
+      produce<S, G>(a, sp.bars, ntask, ncols, [&](int g, int st, const Cursor &cu) {
         const int k = g * S + st;
         int s = 0;
 #pragma unroll
         for (int gg = 0; gg < G; ++gg)
           if (gg == g) s = su[gg];
-        const bool done = sus_issue<Q, DMAX, MARKOV>(a, task, s, lvl_begin, ncols, sp.hdr + (size_t)k * kHdr,
+        const bool done = sus_issue<Q, DMAX, MARKOV>(a, cu.fb, cu.item, s, lvl_begin, sp.hdr + (size_t)k * kHdr,
                                                      sp.pay + (size_t)k * Sh::PAYA,
                                                      sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k);
 #pragma unroll
@@ -1193,14 +1253,14 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
   long long lo, hi;
   group_range(ntask, (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
   // producer cursor over (task, unit) of this group
-  long long ptask = lo;
-  int pu = 0, pissued = 0;
+  Cursor pc;
+  int pu = 0;
+  if (producer) pc.init(a, lo, hi, ncols);
   auto issue_next = [&](int k) {
-    if (ptask >= hi) return;
-    if (sus_issue<Q, DMAX, MARKOV>(a, ptask, pu, lvl_begin, ncols, sp.hdr + (size_t)k * kHdr,
+    if (!pc.valid()) return;
+    if (sus_issue<Q, DMAX, MARKOV>(a, pc.fb, pc.item, pu, lvl_begin, sp.hdr + (size_t)k * kHdr,
                                    sp.pay + (size_t)k * Sh::PAYA, sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k))
-      ++ptask;
-    ++pissued;
+      pc.advance(a);
   };
   if (producer)
     for (int n = 0; n < S; ++n) issue_next(g * S + n);
@@ -1215,7 +1275,7 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       const uint32_t pay_u32 = sp.pay_u32 + (uint32_t)((size_t)k * Sh::PAYA);
       uint64_t *empty = sp.bars + G * S + k;
       auto refill = [&]() {
-        if (producer && ptask < hi) {
+        if (producer && pc.valid()) {
           mbar_wait(empty, (uint32_t)((rr / S) & 1));
           issue_next(k);
         }
@@ -1276,7 +1336,6 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       group_bar<T>(g);  // transpose / reduction scratch and rsm free
     }
   }
-  (void)pissued;
 }
 
 // ============================================================== launchers
@@ -1317,7 +1376,7 @@ constexpr int stages_fit(int want) {
 
 template <int Q, int DM>
 static int cn_launch(const WaveArgs &a, cudaStream_t s) {
-  constexpr int KR = KRof<Q, KCN>::v, T = Q / KR, G = Gof<T>::v;
+  constexpr int KR = KRof<Q, KCN>::v, T = Q / KR, G = Gof<T, KCN>::v;
   constexpr int NS = stages_fit<CNShape<Q, KR, DM, 1, G>, CNShape<Q, KR, DM, 2, G>>(GFQ_STAGES_CN);
   using CS = CNShape<Q, KR, DM, NS, G>;
   if (CS::SMEM > 232448) return too_big("k_cn");
@@ -1334,7 +1393,7 @@ static int cn_q(const WaveArgs &a, cudaStream_t s) {
 
 template <int Q, int DV, bool MK>
 static int vn_launch(const WaveArgs &a, int clip, cudaStream_t s) {
-  constexpr int KR = KRof<Q, KVN>::v, T = Q / KR, G = Gof<T>::v;
+  constexpr int KR = KRof<Q, KVN>::v, T = Q / KR, G = Gof<T, KVN>::v;
   constexpr int NS = stages_fit<VNShape<Q, KR, DV, MK, 1, G>, VNShape<Q, KR, DV, MK, 2, G>>(GFQ_STAGES_VN);
   using VS = VNShape<Q, KR, DV, MK, NS, G>;
   if (VS::SMEM > 232448) return too_big("k_vn");
@@ -1353,7 +1412,7 @@ static int vn_q(const WaveArgs &a, int clip, cudaStream_t s) {
 
 template <int Q, int DM, int DV, bool MK>
 static int sus_launch(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
-  constexpr int KR = KRof<Q, KSUS>::v, T = Q / KR, G = Gof<T>::v;
+  constexpr int KR = KRof<Q, KSUS>::v, T = Q / KR, G = Gof<T, KSUS>::v;
   constexpr int NS =
       stages_fit<SUSShape<Q, KR, DM, DV, MK, 1, G>, SUSShape<Q, KR, DM, DV, MK, 2, G>>(GFQ_STAGES_SUS);
   using SS = SUSShape<Q, KR, DM, DV, MK, NS, G>;
