@@ -1,0 +1,94 @@
+"""Table-1-style convergence statistics on the GPU (Table 1):
+per config (and Eb/N0 point), PUS and SUS decoded with early exit on the same
+frames; paired ratio statistics over frames where both converge (reading A29).
+usage: ratio_table.py [frames] > table.json"""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import synth
+from paper_cs_0605069_b200 import gfq
+
+nf = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+calibrate = "--calibrate" in sys.argv
+rows = []
+
+
+def run_point(name, cfg, code, gc, T, F, point=0, param=None):
+    if param is None:
+        fr = synth.frames_for(cfg, code, range(F), point=point)
+    else:
+        fr = synth.make_frames(code, cfg.cid, range(F), cfg.source, cfg.channel, param, stay=cfg.stay, point=99)
+    ch = {synth.BSC: gfq.GFQ_BSC, synth.BEC: gfq.GFQ_BEC, synth.BIAWGN: gfq.GFQ_BIAWGN}[fr.channel]
+    obs = torch.as_tensor(fr.obs).cuda()
+    res = {}
+    for sch in (gfq.GFQ_PUS, gfq.GFQ_SUS):
+        prm = gfq.Params(ch, fr.ch_param, sch, cfg.max_iters, early_exit=True, markov_T=T)
+        s, it, _ = gfq.gfq_decode(gc, obs, prm)
+        it = it.cpu().numpy(); s = s.cpu().numpy()
+        res[sch] = (it, (s != fr.s).any(axis=1), (s != fr.s).mean())
+    return fr, res
+
+
+if calibrate:
+    # supplementary near-threshold points: the channel parameter
+    # found by bisection so that the mean PUS iteration count is ~45 (Table 1's regime)
+    for name in ["C2", "C4"]:
+        cfg = synth.CONFIGS[name]
+        code = synth.code_for(cfg)
+        gc = gfq.Code.from_synth(code)
+        T = synth.markov_T_for(cfg)
+        lo, hi = cfg.ch_params[0], 0.5 if cfg.channel == synth.BSC else 0.95
+        for _ in range(14):
+            mid = 0.5 * (lo + hi)
+            fr, res = run_point(name, cfg, code, gc, T, 256, param=mid)
+            tp = res[0][0]
+            ok = tp > 0
+            mean = tp[ok].mean() if ok.mean() > 0.5 else 1e9
+            if mean < 45:
+                lo = mid
+            else:
+                hi = mid
+        param = lo
+        fr, res = run_point(name, cfg, code, gc, T, nf, param=param)
+        tp, ts = res[0][0], res[1][0]
+        both = (tp > 0) & (ts > 0)
+        q = ts[both] / tp[both]
+        r = dict(config=name + "-near-threshold (supplementary)", channel=synth.CHANNEL_NAMES[cfg.channel],
+                 q=cfg.q, source=cfg.source, noise=param, frames=nf, paired=int(both.sum()),
+                 mean_t_sus=float(ts[both].mean()), mean_t_pus=float(tp[both].mean()),
+                 nonconv_pus=int((tp < 0).sum()), nonconv_sus=int((ts < 0).sum()),
+                 ratio_of_means=float(ts[both].mean() / tp[both].mean()), mean_ratio=float(q.mean()),
+                 std_ratio=float(q.std()))
+        print(json.dumps(r), flush=True)
+    sys.exit(0)
+for name in ["C1", "C2", "C3", "C4", "C5"]:
+    cfg = synth.CONFIGS[name]
+    code = synth.code_for(cfg)
+    gc = gfq.Code.from_synth(code)
+    T = synth.markov_T_for(cfg)
+    for point in range(len(cfg.ch_params)):
+        F = min(nf, cfg.frames)
+        fr = synth.frames_for(cfg, code, range(F), point=point)
+        ch = {synth.BSC: gfq.GFQ_BSC, synth.BEC: gfq.GFQ_BEC, synth.BIAWGN: gfq.GFQ_BIAWGN}[fr.channel]
+        obs = torch.as_tensor(fr.obs).cuda()
+        res = {}
+        for sch in (gfq.GFQ_PUS, gfq.GFQ_SUS):
+            prm = gfq.Params(ch, fr.ch_param, sch, cfg.max_iters, early_exit=True, markov_T=T)
+            s, it, _ = gfq.gfq_decode(gc, obs, prm)
+            it = it.cpu().numpy(); s = s.cpu().numpy()
+            res[sch] = (it, (s != fr.s).any(axis=1), (s != fr.s).mean())
+        tp, ts = res[0][0], res[1][0]
+        both = (tp > 0) & (ts > 0)
+        r = dict(config=name, channel=synth.CHANNEL_NAMES[cfg.channel], q=cfg.q, source=cfg.source,
+                 noise=cfg.ch_params[point], frames=F, paired=int(both.sum()),
+                 mean_t_sus=float(ts[both].mean()) if both.any() else None,
+                 mean_t_pus=float(tp[both].mean()) if both.any() else None,
+                 nonconv_pus=int((tp < 0).sum()), nonconv_sus=int((ts < 0).sum()),
+                 fer_pus=float(res[0][1].mean()), fer_sus=float(res[1][1].mean()),
+                 ser_pus=float(res[0][2]), ser_sus=float(res[1][2]))
+        if both.any():
+            q = ts[both] / tp[both]
+            r.update(ratio_of_means=float(ts[both].mean() / tp[both].mean()), mean_ratio=float(q.mean()),
+                     std_ratio=float(q.std()))
+        rows.append(r)
+        print(json.dumps(r), flush=True)
