@@ -617,6 +617,34 @@ __device__ __forceinline__ void xpose(double (&u)[D][KR], double *buf, int &m, i
   }
 }
 
+// Layout switch of D messages two at a time, alternating between buffer X0
+// (the task's own, already-consumed input stage) and X1 (the group scratch):
+// one barrier per pair.  t counts the pair transposes of the task (starts at
+// 1 -> X1 in the forward direction, continues in the inverse one, so the
+// stage is first overwritten after a barrier, and a task always ends on X0
+// and starts on X1: no other barrier is needed across tasks).
+template <int Q, int KR, int D, bool A2B>
+__device__ __forceinline__ void xpose_pairs(double (&u)[D][KR], double *X0, double *X1, int &t, int g, int c,
+                                            int lane) {
+  constexpr int T = Q / KR;
+#pragma unroll
+  for (int p0 = 0; p0 < D; p0 += 2) {
+    double *b = (t & 1) ? X1 : X0;
+    ++t;
+#pragma unroll
+    for (int s = p0; s < p0 + 2 && s < D; ++s)
+#pragma unroll
+      for (int k = 0; k < KR; ++k)
+        b[((size_t)(s - p0) * Q + (A2B ? idxA<Q, KR>(c, k) : idxB<Q, KR>(c, k))) * 32 + lane] = u[s][k];
+    group_bar<T>(g);
+#pragma unroll
+    for (int s = p0; s < p0 + 2 && s < D; ++s)
+#pragma unroll
+      for (int k = 0; k < KR; ++k)
+        u[s][k] = b[((size_t)(s - p0) * Q + (A2B ? idxB<Q, KR>(c, k) : idxA<Q, KR>(c, k))) * 32 + lane];
+  }
+}
+
 // ping-pong transposes for large fields (tuning knob)
 #ifndef GFQ_PP_MINQ
 #define GFQ_PP_MINQ 32
@@ -625,6 +653,10 @@ template <int Q>
 struct PPof {
   static constexpr bool v = Q >= GFQ_PP_MINQ;
 };
+// check node: pair transposes through the consumed input stage (large fields)
+#ifndef GFQ_CN_PAIRS
+#define GFQ_CN_PAIRS 1
+#endif
 
 // ============================================================== shared-memory layout
 // [mbarriers][G*S headers of kHdr][pad][G*S payload slots, each a multiple of
@@ -782,10 +814,12 @@ __device__ __forceinline__ void cn_issue(const WaveArgs &a, int fb, int i, unsig
 // round-off is clamped to 0 (reading A20).
 template <int Q, int KR, int D, int DMAX, typename RF>
 __device__ __forceinline__ void cn_task(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_u32,
-                                        uint64_t *empty, double *xp, int &m, int g, int c, int lane, RF &&refill) {
+                                        double *stage_x, uint64_t *empty, double *xp, int &m, int g, int c,
+                                        int lane, RF &&refill) {
   using C = QC<Q, KR>;
   constexpr int T = C::T, LKR = C::LKR, LT = C::LT, P = C::P;
   constexpr bool PP = PPof<Q>::v;
+  constexpr bool PAIRS = PP && GFQ_CN_PAIRS && (T > 1);
   const TaskInfo ti = *(const TaskInfo *)hdr;
   const CheckDesc *cd = (const CheckDesc *)(hdr + 128);
   const int fb = ti.fb;
@@ -805,11 +839,20 @@ __device__ __forceinline__ void cn_task(const WaveArgs &a, const unsigned char *
 #pragma unroll
     for (int k = 0; k < KR; ++k) u[s][k] = (double)lds_f32(ad[k]);
   }
-  release_stage(empty, lane);
-  refill();
+  if constexpr (!PAIRS) {
+    release_stage(empty, lane);
+    refill();
+  }
+  // pair-transpose counter (PAIRS): start on X1 so that the stage (X0) is only
+  // overwritten after the first barrier, when every warp has read its inputs
+  int tp = 1;
 #pragma unroll
   for (int s = 0; s < D; ++s) wht_bits<KR, 0, LKR>(u[s]);
-  if constexpr (T > 1) {
+  if constexpr (PAIRS) {
+    xpose_pairs<Q, KR, D, true>(u, stage_x, xp, tp, g, c, lane);
+#pragma unroll
+    for (int s = 0; s < D; ++s) wht_bits<KR, LKR - LT, LKR>(u[s]);
+  } else if constexpr (T > 1) {
     xpose<Q, KR, D, PP, true>(u, xp, m, g, c, lane);
 #pragma unroll
     for (int s = 0; s < D; ++s) wht_bits<KR, LKR - LT, LKR>(u[s]);
@@ -817,7 +860,13 @@ __device__ __forceinline__ void cn_task(const WaveArgs &a, const unsigned char *
   uint32_t sm[KR];
   sign_masks<KR, T>(z, c, sm);
   loo_signed<D, KR, D>(u, sm);
-  if constexpr (T > 1) {
+  if constexpr (PAIRS) {
+#pragma unroll
+    for (int s = 0; s < D; ++s) wht_bits<KR, LKR - LT, LKR>(u[s]);
+    xpose_pairs<Q, KR, D, false>(u, stage_x, xp, tp, g, c, lane);
+    release_stage(empty, lane);  // the stage served as transpose buffer X0
+    refill();
+  } else if constexpr (T > 1) {
 #pragma unroll
     for (int s = 0; s < D; ++s) wht_bits<KR, LKR - LT, LKR>(u[s]);
     if constexpr (!PP) group_bar<T>(g);  // bulk buffer: all forward reads done
@@ -893,17 +942,17 @@ __global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(Wave
     mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
     const int d = ((const TaskInfo *)hdr)->deg;
     switch (d) {
-      case 1: cn_task<Q, KR, 1, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane, refill); break;
-      case 2: cn_task<Q, KR, 2, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane, refill); break;
-      case 3: cn_task<Q, KR, 3, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane, refill); break;
-      case 4: cn_task<Q, KR, 4, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane, refill); break;
+      case 1: cn_task<Q, KR, 1, DMAX>(a, hdr, pay, (double *)(sp.pay + (size_t)k * Sh::PAYA), empty, xp, m, g, c, lane, refill); break;
+      case 2: cn_task<Q, KR, 2, DMAX>(a, hdr, pay, (double *)(sp.pay + (size_t)k * Sh::PAYA), empty, xp, m, g, c, lane, refill); break;
+      case 3: cn_task<Q, KR, 3, DMAX>(a, hdr, pay, (double *)(sp.pay + (size_t)k * Sh::PAYA), empty, xp, m, g, c, lane, refill); break;
+      case 4: cn_task<Q, KR, 4, DMAX>(a, hdr, pay, (double *)(sp.pay + (size_t)k * Sh::PAYA), empty, xp, m, g, c, lane, refill); break;
       default:
         if constexpr (DMAX > 4) {
           switch (d) {
-            case 5: cn_task<Q, KR, 5, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane, refill); break;
-            case 6: cn_task<Q, KR, 6, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane, refill); break;
-            case 7: cn_task<Q, KR, 7, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane, refill); break;
-            default: cn_task<Q, KR, 8, DMAX>(a, hdr, pay, empty, xp, m, g, c, lane, refill); break;
+            case 5: cn_task<Q, KR, 5, DMAX>(a, hdr, pay, (double *)(sp.pay + (size_t)k * Sh::PAYA), empty, xp, m, g, c, lane, refill); break;
+            case 6: cn_task<Q, KR, 6, DMAX>(a, hdr, pay, (double *)(sp.pay + (size_t)k * Sh::PAYA), empty, xp, m, g, c, lane, refill); break;
+            case 7: cn_task<Q, KR, 7, DMAX>(a, hdr, pay, (double *)(sp.pay + (size_t)k * Sh::PAYA), empty, xp, m, g, c, lane, refill); break;
+            default: cn_task<Q, KR, 8, DMAX>(a, hdr, pay, (double *)(sp.pay + (size_t)k * Sh::PAYA), empty, xp, m, g, c, lane, refill); break;
           }
         } else {
           release_stage(empty, lane);  // d == 0: an empty check has no edge
