@@ -206,3 +206,73 @@ def test_natural_chain_labelling_many_levels(gfq):
     ref = oc.decode(hard, pi, schedule=1, max_iters=5, fixed=True, T=T, keep_messages=True)
     assert float(np.max(np.abs(qg.cpu().numpy() - ref["q"]))) <= MSG_TOL
     assert float(np.max(np.abs(Qg.cpu().numpy() - ref["Q"]))) <= MSG_TOL
+
+
+def _random_code(p, N, M, colw, seed):
+    """A generic (non-MN-chain) code with larger check and variable degrees:
+    exercises the degree-8 kernel variants."""
+    rng = np.random.default_rng(seed)
+    q = 1 << p
+    Ar, Ac = [], []
+    for j in range(N):
+        for i in rng.choice(M, colw, replace=False):
+            Ar.append(i); Ac.append(j)
+    Br, Bc = [], []
+    for j in range(M):
+        for i in rng.choice(M, 2, replace=False):
+            Br.append(i); Bc.append(j)
+    A = (np.array(Ar, np.int32), np.array(Ac, np.int32), rng.integers(1, q, len(Ar)).astype(np.uint8))
+    B = (np.array(Br, np.int32), np.array(Bc, np.int32), rng.integers(1, q, len(Br)).astype(np.uint8))
+    return A, B
+
+
+@pytest.mark.parametrize("p", [2, 4, 6])
+def test_high_degree_code_message_parity(gfq, p):
+    """Check degree up to ~8 and variable degree 5: the DMAX = DVMAX = 8 kernels
+    (or a clean GFQ_EUNSUPPORTED where shared memory cannot hold them)."""
+    N, M = 40, 64
+    for seed in range(100 + p, 200 + p):   # a draw with max check degree in 5..8
+        A, B = _random_code(p, N, M, 4, seed)
+        rows = np.concatenate([A[0], B[0]]); cols = np.concatenate([A[1], B[1] + N])
+        vals = np.concatenate([A[2], B[2]])
+        deg = np.bincount(rows, minlength=M)
+        if 4 < deg.max() <= 8:
+            break
+    assert 4 < deg.max() <= 8
+    gcode = gfq.Code(p, synth.PRIM_POLY[p], N, M, *A, *B)
+    oc = oracle.OCode(p, synth.PRIM_POLY[p], N, M, rows, cols, vals)
+    rng = np.random.default_rng(p)
+    F = 40
+    hard = rng.integers(0, 2, (F, M * p)).astype(np.uint8)
+    pi = rng.uniform(0.02, 0.3, (F, M * p)).astype(np.float32)
+    for schedule in (0, 1):
+        prm = gfq.Params(schedule=schedule, max_iters=4, early_exit=False, keep_messages=True)
+        try:
+            x, it, ws = gfq.gfq_decode_evidence(gcode, torch.as_tensor(hard).cuda(), torch.as_tensor(pi).cuda(), prm)
+        except gfq.GfqError as e:
+            assert e.code == gfq.GFQ_EUNSUPPORTED and "shared memory" in str(e)
+            continue
+        qg, rg, Qg = gfq.gfq_export_messages(gcode, F, ws, prm)
+        ref = oc.decode(hard, pi.astype(np.float64), schedule=schedule, max_iters=4, fixed=True, keep_messages=True)
+        assert float(np.max(np.abs(qg.cpu().numpy() - ref["q"]))) <= MSG_TOL
+        assert float(np.max(np.abs(rg.cpu().numpy() - ref["r"]))) <= MSG_TOL
+        assert float(np.max(np.abs(Qg.cpu().numpy() - ref["Q"]))) <= MSG_TOL
+        assert np.array_equal(it.cpu().numpy(), ref["iters"])
+
+
+def test_markov_sus_pus_full_c2_sampled_decisions(gfq):
+    """Markov source (Eq. 7 on the GPU vs Eq. 6 in the oracle) with early exit on a
+    BSC at a noisier point than C2 (more iterations, more prior updates)."""
+    cfg = synth.CONFIGS["C2"]
+    code = synth.code_for(cfg)
+    fr = synth.make_frames(code, cfg.cid, range(96), "markov", synth.BSC, 0.12, stay=cfg.stay, point=7)
+    T = synth.markov_T_for(cfg)
+    gcode = gfq.Code.from_synth(code)
+    oc = oracle.OCode.from_synth(code)
+    hard, pi = oracle.frontend(fr.channel, fr.ch_param, fr.obs)
+    for schedule in (0, 1):
+        _, s_hat, iters, ws = _gpu_decode(gfq, gcode, fr, schedule, cfg.max_iters, True, T)
+        ref = oc.decode(hard, pi, schedule=schedule, max_iters=cfg.max_iters, T=T)
+        match, _ = _decision_match(s_hat, iters, ref["xhat"][:, :code.N], ref["iters"])
+        assert int((~match).sum()) == 0
+        assert (iters > 3).mean() > 0.5   # the noisier point really iterates
