@@ -151,6 +151,19 @@ __device__ __forceinline__ void group_bar(int g) {
     asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(T * 32) : "memory");
   }
 }
+// One-sided group barrier on a second id per group (15 - g; ids 1..G are the
+// group_bar ones): warp `waiter` waits until every other warp of the group has
+// arrived; the others only arrive and run on.  Safe to reuse because every
+// waiter passes a full group_bar before the next round of arrivals.
+template <int T>
+__device__ __forceinline__ void group_gather(int g, bool waiter) {
+  if constexpr (T > 1) {
+    if (waiter)
+      asm volatile("bar.sync %0, %1;" ::"r"(15 - g), "r"(T * 32) : "memory");
+    else
+      asm volatile("bar.arrive %0, %1;" ::"r"(15 - g), "r"(T * 32) : "memory");
+  }
+}
 
 // ============================================================== small helpers
 // In-register WHT butterflies over bits [LO, HI) of the register index.
@@ -532,11 +545,14 @@ __device__ __forceinline__ void vn_core(const WaveArgs &a, int fb, int j, const 
   for (int k = KR - 1; k >= 0; --k)
     if (tot[k] >= thr) bidx = c * KR + k;
   if constexpr (T > 1) {
+    // only warp 0 needs the index (it writes the estimate): the others arrive and go on
     int *ired = (int *)(red + (size_t)(NS + 1) * T * 32 + (size_t)(NS + 1) * 32);
     ired[c * 32 + lane] = bidx;
-    group_bar<T>(g);
+    group_gather<T>(g, c == 0);
+    if (c == 0) {
 #pragma unroll
-    for (int cc = 0; cc < T; ++cc) bidx = min(bidx, ired[cc * 32 + lane]);
+      for (int cc = 1; cc < T; ++cc) bidx = min(bidx, ired[cc * 32 + lane]);
+    }
   }
   if (bidx >= Q) bidx = 0;
   int bad = 0;
@@ -1094,7 +1110,7 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
         break;
     }
 #undef VT
-    if constexpr (T > 1) group_bar<T>(g);  // red reusable
+    // no barrier here: vn_core's own barriers order every reuse of red
   }
 }
 
@@ -1214,14 +1230,14 @@ __device__ __forceinline__ void sus_check(const WaveArgs &a, const unsigned char
   perm_addrs<P, LKR, KR>(0u, pke, c, ad, rh);  // ad[k] = (h_e^-1 y) * 128: a = h_e^-1 y
   const int s = ti.s;
   unsigned char *rs = (unsigned char *)(rsm + (size_t)s * Q * 32 + lane);
-  unsigned char *rdst =
-      (a.rmsg && !frozen) ? (unsigned char *)(a.rmsg + ((size_t)ti.fb * a.c.E + ti.e0 + s) * Q * 32 + lane)
-                          : nullptr;
 #pragma unroll
-  for (int k = 0; k < KR; ++k) {
-    const float fv = fmaxf((float)acc[0][k], 0.0f);
-    *(float *)(rs + ad[k]) = fv;
-    if (rdst) *(float *)(rdst + ad[k]) = fv;
+  for (int k = 0; k < KR; ++k) *(float *)(rs + ad[k]) = fmaxf((float)acc[0][k], 0.0f);
+  if (a.rmsg != nullptr) {  // keep_messages only (export): warp-uniform branch
+    if (!frozen) {
+      unsigned char *rdst = (unsigned char *)(a.rmsg + ((size_t)ti.fb * a.c.E + ti.e0 + s) * Q * 32 + lane);
+#pragma unroll
+      for (int k = 0; k < KR; ++k) *(float *)(rdst + ad[k]) = fmaxf((float)acc[0][k], 0.0f);
+    }
   }
 }
 
@@ -1381,8 +1397,13 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
             break;
         }
 #undef SV
+        if constexpr (SS::PP && SS::RED_D <= (size_t)Q * 32) m = 1;  // next transpose avoids red (buffer 0)
       }
-      group_bar<T>(g);  // transpose / reduction scratch and rsm free
+      // Ping-pong transposes need no barrier between units (rsm slots are
+      // distinct; the next rsm write follows a transpose barrier), and after
+      // the variable update the next transpose writes buffer 1 while the
+      // reduction scratch lives in buffer 0.  Bulk mode reuses its buffers.
+      if constexpr (!SS::PP || SS::RED_D > (size_t)Q * 32) group_bar<T>(g);
     }
   }
 }
