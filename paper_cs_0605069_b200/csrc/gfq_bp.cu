@@ -298,6 +298,28 @@ __device__ __forceinline__ void perm_addrs(uint32_t base, unsigned long long pk,
   for (int k = 0; k < KR; ++k) ad[k] = b0 ^ ((uint32_t)row_lo<P, LKR>(bb, k) << 7);
 }
 
+// The same addresses from the per-field table rowtab[a][y] = (a*y) << 7 (a =
+// h^-1, the low byte of the packed basis): one uniform 2*KR-byte load (L1
+// broadcast) and one add per entry.
+template <int Q, int KR>
+__device__ __forceinline__ void tab_addrs(uint32_t base, const unsigned short *rowtab, unsigned long long pk, int c,
+                                          uint32_t (&ad)[KR]) {
+  static_assert(KR == 2 || KR == 4 || KR == 8, "tab_addrs: KR");
+  const unsigned short *p = rowtab + (size_t)(pk & 0xff) * Q + c * KR;
+  uint32_t w[KR / 2];
+  if constexpr (KR == 8) {
+    const uint4 v = __ldg((const uint4 *)p);
+    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+  } else if constexpr (KR == 4) {
+    const uint2 v = __ldg((const uint2 *)p);
+    w[0] = v.x; w[1] = v.y;
+  } else {
+    w[0] = __ldg((const unsigned int *)p);
+  }
+#pragma unroll
+  for (int k = 0; k < KR; ++k) ad[k] = base + ((k & 1) ? (w[k >> 1] >> 16) : (w[k >> 1] & 0xffffu));
+}
+
 // ============================================================== leave-one-out with the syndrome sign
 // out_s = sign * prod_{s' != s} u_s'   for exact degree D (sign folded in as an
 // XOR of the high word: the same sign multiplies every output at frequency w).
@@ -1190,8 +1212,7 @@ __device__ __forceinline__ void sus_check(const WaveArgs &a, const unsigned char
 #pragma unroll
   for (int t = 0; t < DO; ++t) {
     uint32_t ad[KR];
-    int rh;
-    perm_addrs<P, LKR, KR>(pay_u32 + (uint32_t)(t * Q * 128 + lane * 4), sd->perm_o[t], c, ad, rh);
+    tab_addrs<Q, KR>(pay_u32 + (uint32_t)(t * Q * 128 + lane * 4), a.c.rowtab, sd->perm_o[t], c, ad);
 #pragma unroll
     for (int k = 0; k < KR; ++k) v[t][k] = (double)lds_f32(ad[k]);
   }
@@ -1226,8 +1247,7 @@ __device__ __forceinline__ void sus_check(const WaveArgs &a, const unsigned char
   }
   wht_bits<KR, 0, LKR>(acc[0]);
   uint32_t ad[KR];
-  int rh;
-  perm_addrs<P, LKR, KR>(0u, pke, c, ad, rh);  // ad[k] = (h_e^-1 y) * 128: a = h_e^-1 y
+  tab_addrs<Q, KR>(0u, a.c.rowtab, pke, c, ad);  // ad[k] = (h_e^-1 y) * 128: a = h_e^-1 y
   const int s = ti.s;
   unsigned char *rs = (unsigned char *)(rsm + (size_t)s * Q * 32 + lane);
 #pragma unroll

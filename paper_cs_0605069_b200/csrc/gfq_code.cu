@@ -204,6 +204,9 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   std::vector<unsigned char> mul((size_t)q * q);
   for (int x = 0; x < q; ++x)
     for (int y = 0; y < q; ++y) mul[x * q + y] = (unsigned char)gf.mul(x, y);
+  std::vector<unsigned short> rowtab((size_t)q * q);
+  for (int x = 0; x < q; ++x)
+    for (int y = 0; y < q; ++y) rowtab[x * q + y] = (unsigned short)(gf.mul(x, y) << 7);
 
   // one device blob
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -219,6 +222,7 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   const size_t o_lptr = off; off += al(sizeof(int) * (nlev + 1));
   const size_t o_lcol = off; off += al(sizeof(int) * V);
   const size_t o_mul = off; off += al((size_t)q * q);
+  const size_t o_rowtab = off; off += al((size_t)q * q * 2);
   const size_t o_cdesc = off; off += al(sizeof(CheckDesc) * M);
   const size_t o_vdesc = off; off += al(sizeof(VarDesc) * V);
   const size_t o_sdesc = off; off += al(sizeof(SusDesc) * E);
@@ -237,6 +241,7 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   put(o_lptr, level_ptr.data(), sizeof(int) * (nlev + 1));
   put(o_lcol, level_cols.data(), sizeof(int) * V);
   put(o_mul, mul.data(), (size_t)q * q);
+  put(o_rowtab, rowtab.data(), (size_t)q * q * 2);
   put(o_cdesc, cdesc.data(), sizeof(CheckDesc) * M);
   put(o_vdesc, vdesc.data(), sizeof(VarDesc) * V);
   put(o_sdesc, sdesc.data(), sizeof(SusDesc) * E);
@@ -272,6 +277,7 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   c->d.level_ptr = (const int *)(b + o_lptr);
   c->d.level_cols = (const int *)(b + o_lcol);
   c->d.mul = b + o_mul;
+  c->d.rowtab = (const unsigned short *)(b + o_rowtab);
   c->d.check_desc = (const CheckDesc *)(b + o_cdesc);
   c->d.var_desc = (const VarDesc *)(b + o_vdesc);
   c->d.sus_desc = (const SusDesc *)(b + o_sdesc);

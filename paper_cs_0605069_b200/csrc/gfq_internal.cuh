@@ -60,6 +60,7 @@ struct DevCode {
   const int *level_ptr;      // [L+1]   SUS dependency levels
   const int *level_cols;     // [V]
   const unsigned char *mul;  // [q*q]   GF(2^p) product table
+  const unsigned short *rowtab;  // [q*q] (a * y) << 7: byte offset of row a*y of a q x 128 B message
   const CheckDesc *check_desc;  // [M]
   const VarDesc *var_desc;      // [V]
   const SusDesc *sus_desc;      // [E] canonical order
