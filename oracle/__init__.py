@@ -60,7 +60,7 @@ def lib():
             L.o_unsatisfied.argtypes = [vp, vp, vp]
             L.o_unsatisfied.restype = i
             L.o_decode_frame.argtypes = [vp, i, i, i, vp, vp, vp, vp, vp, P(i), vp, vp, vp,
-                                         P(ctypes.c_long)]
+                                         P(ctypes.c_long), vp, vp]
             L.o_decode_frame.restype = i
             _lib = L
     return _lib
@@ -170,10 +170,12 @@ class OCode:
         return lib().o_unsatisfied(self._h, _p(x), _p(z))
 
     def decode(self, hard, pi, schedule: int = PUS, max_iters: int = 100, fixed: bool = False,
-               T=None, pi0=None, keep_messages: bool = False, threads: int = 0):
+               T=None, pi0=None, keep_messages: bool = False, threads: int = 0, s_true=None):
         """Decode frames. hard uint8 [F][M*p], pi float64 [F][M*p] (fp32 values may be
         passed: they are widened exactly).  Returns dict(xhat [F][V], iters [F],
-        zero_norms [F], and q/r [F][E][q], Q [F][V][q] if keep_messages)."""
+        zero_norms [F], and q/r [F][E][q], Q [F][V][q] if keep_messages; with the true
+        sources s_true uint8 [F][N] also trace [F][max_iters+1], the correct source
+        bits of the estimate after each iteration (Fig. 1))."""
         hard = np.ascontiguousarray(hard, dtype=np.uint8)
         pi = np.ascontiguousarray(pi, dtype=np.float64)
         F = hard.shape[0]
@@ -186,6 +188,8 @@ class OCode:
         Qm = np.zeros((F, V, q)) if keep_messages else None
         Tc = None if T is None else np.ascontiguousarray(T, dtype=np.float64)
         p0 = None if pi0 is None else np.ascontiguousarray(pi0, dtype=np.float64)
+        st = None if s_true is None else np.ascontiguousarray(s_true, dtype=np.uint8).reshape(F, self.N)
+        tr = None if s_true is None else np.zeros((F, max(int(max_iters), 0) + 1), np.int32)
         L = lib()
 
         def one(f):
@@ -195,7 +199,8 @@ class OCode:
                              _p(hard[f]), _p(pi[f]), _p(Tc), _p(p0), _p(xhat[f]), ctypes.byref(it),
                              _p(qm[f]) if keep_messages else None,
                              _p(rm[f]) if keep_messages else None,
-                             _p(Qm[f]) if keep_messages else None, ctypes.byref(z))
+                             _p(Qm[f]) if keep_messages else None, ctypes.byref(z),
+                             None if st is None else _p(st[f]), None if tr is None else _p(tr[f]))
             iters[f] = it.value
             zn[f] = z.value
 
@@ -209,4 +214,6 @@ class OCode:
         out = dict(xhat=xhat, iters=iters, zero_norms=zn, threads=min(nthreads, max(F, 1)))
         if keep_messages:
             out.update(q=qm, r=rm, Q=Qm)
+        if tr is not None:
+            out["trace"] = tr
         return out

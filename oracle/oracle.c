@@ -344,6 +344,18 @@ static int var_edge(const ocode *c, long e, const double *prior_j, const double 
     return o_var_node(q, dv, prior_j, rmsg + (size_t)e0 * q, (int)(e - e0), qout);
 }
 
+/* Number of source bits of x (symbols 0..N-1, p bits each, A2) equal to the
+ * true source s: the "percentage of correct bits" of Fig. 1 times
+ * N*p/100. */
+static int correct_source_bits(int p, int N, const uint8_t *x, const uint8_t *s)
+{
+    int ok = 0;
+    for (int j = 0; j < N; ++j)
+        for (int b = 0; b < p; ++b)
+            ok += ((x[j] >> b) & 1) == ((s[j] >> b) & 1);
+    return ok;
+}
+
 /* One frame, start to finish.
  *   schedule: 0 = PUS, 1 = SUS
  *   hard[M*p], pi[M*p]: front-end output (bits LSB first, A2)
@@ -354,12 +366,17 @@ static int var_edge(const ocode *c, long e, const double *prior_j, const double 
  *   xhat[V] out; *iters out: first passing t in 1..max_iters or -1 (A21).
  *   qmsg/rmsg [E*q], Qpost [V*q]: optional (NULL) final messages, canonical order.
  *   *zero_norms: count of vanished normalisers (A19; should stay 0).
+ *   s_true[N] / trace[max_iters+1]: optional (NULL) instrumentation of Fig. 1
+ *          (P:296-317): trace[t] = number of source BITS of the estimate x^(t)
+ *          equal to the true source s (t = 0: the clipped priors; t >= 1: after
+ *          iteration t).  After an early exit at t0 the estimate is frozen, so
+ *          trace[t] = trace[t0] for t > t0.
  */
 int o_decode_frame(const ocode *c, int schedule, int max_iters, int fixed,
                    const uint8_t *hard, const double *pi, const double *T,
                    const double *pi0_in, uint8_t *xhat, int *iters,
                    double *qmsg_out, double *rmsg_out, double *Q_out,
-                   long *zero_norms)
+                   long *zero_norms, const uint8_t *s_true, int *trace)
 {
     const int p = c->p, q = c->q, N = c->N, M = c->M, V = c->V;
     const long E = c->E;
@@ -397,7 +414,7 @@ int o_decode_frame(const ocode *c, int schedule, int max_iters, int fixed,
         memcpy(qmsg + (size_t)e * q, prior + (size_t)c->edge_col[e] * q, sizeof(double) * (size_t)q);
 
     *iters = -1;
-    if (max_iters <= 0) { /* clip the priors */
+    if (max_iters <= 0 || trace) { /* clip the priors: the estimate x^(0) */
         for (int j = 0; j < V; ++j) {
             const double *pj = prior + (size_t)j * q;
             double mx = 0.0;
@@ -406,8 +423,15 @@ int o_decode_frame(const ocode *c, int schedule, int max_iters, int fixed,
             int best = 0;
             for (int a = 0; a < q; ++a)
                 if (pj[a] >= mx * (1.0 - O_TIE_REL)) { best = a; break; }
-            xhat[j] = (uint8_t)best;
-            memcpy(Q + (size_t)j * q, prior + (size_t)j * q, sizeof(double) * (size_t)q);
+            x[j] = (uint8_t)best;
+            if (max_iters <= 0) {
+                xhat[j] = (uint8_t)best;
+                memcpy(Q + (size_t)j * q, prior + (size_t)j * q, sizeof(double) * (size_t)q);
+            }
+        }
+        if (trace) {
+            trace[0] = correct_source_bits(p, N, x, s_true);
+            for (int t = 1; t <= max_iters; ++t) trace[t] = -1;
         }
     }
     for (int t = 1; t <= max_iters; ++t) {
@@ -436,6 +460,7 @@ int o_decode_frame(const ocode *c, int schedule, int max_iters, int fixed,
                                         Q + (size_t)j * q, &zf);
             zn += zf;
         }
+        if (trace) trace[t] = correct_source_bits(p, N, x, s_true);
         /* Convergence test. */
         int pass = (o_unsatisfied(c, x, z) == 0);
         if (pass && *iters < 0) {
@@ -452,6 +477,9 @@ int o_decode_frame(const ocode *c, int schedule, int max_iters, int fixed,
             free(P);
         }
     }
+    if (trace) /* early exit: the frozen estimate counts for the remaining iterations */
+        for (int t = 1; t <= max_iters; ++t)
+            if (trace[t] < 0) trace[t] = trace[t - 1];
     if (qmsg_out) memcpy(qmsg_out, qmsg, sizeof(double) * (size_t)E * q);
     if (rmsg_out) memcpy(rmsg_out, rmsg, sizeof(double) * (size_t)E * q);
     if (Q_out) memcpy(Q_out, Q, sizeof(double) * (size_t)V * q);

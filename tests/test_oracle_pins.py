@@ -541,3 +541,68 @@ def test_schedule_fixed_points_agree():
             assert np.max(np.abs(res[0][1] - res[1][1])) < 1e-9
             agreed += 1
     assert agreed >= 5
+
+
+# ----------------------------------------------------------------------------- Fig. 1 instrumentation
+def _correct_bits_by_hand(x, s, p):
+    """Correct source bits counted bit by bit from the definition."""
+    n = 0
+    for a, b in zip(x.tolist(), s.tolist()):
+        for k in range(p):
+            n += ((a >> k) & 1) == ((b >> k) & 1)
+    return n
+
+
+@pytest.mark.parametrize("name,schedule", [("C1", oracle.PUS), ("C1", oracle.SUS), ("C2", oracle.SUS)])
+def test_trace_matches_truncated_decodes(name, schedule):
+    """trace[t] (correct source bits after iteration t) equals the count taken by
+    hand on the estimate of a decode stopped after t iterations: x^(t) does not
+    depend on max_iters (the prior refresh after the last iteration only feeds
+    iteration t+1).  After convergence the estimate is frozen."""
+    c = synth.CONFIGS[name]
+    code = synth.code_for(c)
+    fr = synth.frames_for(c, code, range(3))
+    oc = oracle.OCode.from_synth(code)
+    T = synth.markov_T_for(c)
+    hard, pi = oracle.frontend(fr.channel, fr.ch_param, fr.obs)
+    tmax = 12
+    full = oc.decode(hard, pi, schedule=schedule, max_iters=tmax, T=T, s_true=fr.s)
+    tr = full["trace"]
+    assert tr.shape == (3, tmax + 1)
+    for t in range(0, tmax + 1):
+        part = oc.decode(hard, pi, schedule=schedule, max_iters=t, T=T)
+        for f in range(3):
+            it = full["iters"][f]
+            if it > 0 and t > it:
+                assert tr[f, t] == tr[f, it]          # frozen after the early exit
+            else:
+                assert tr[f, t] == _correct_bits_by_hand(part["xhat"][f, :code.N], fr.s[f], code.p)
+    conv = full["iters"] > 0
+    # a converged frame whose estimate is the truth has every bit right
+    for f in np.flatnonzero(conv):
+        if np.array_equal(full["xhat"][f, :code.N], fr.s[f]):
+            assert tr[f, -1] == code.N * code.p
+
+
+def test_trace_point_cases():
+    """Degenerate cases of the count: estimate = truth -> N*p; every bit wrong -> 0."""
+    p, N, M = 2, 2, 2
+    # x0 + x1 + n0 = z0, x1 + n1 = z1 (coefficients 1), noise evidence certain
+    rows = np.array([0, 0, 0, 1, 1], np.int32)
+    cols = np.array([0, 1, 2, 1, 3], np.int32)
+    vals = np.ones(5, np.uint8)
+    oc = oracle.OCode(p, POLY[p], N, M, rows, cols, vals)
+    s = np.array([[1, 2]], np.uint8)
+    # hard bits = t + n with n = 0: z = H [s; 0] = (s0^s1, s1); received t = B^-1 A s here B = I
+    t_sym = np.array([s[0, 0] ^ s[0, 1], s[0, 1]], np.uint8)
+    hard = synth.symbols_to_bits(t_sym[None], p).astype(np.uint8)
+    pi = np.full((1, M * p), 1e-9)
+    out = oc.decode(hard, pi, max_iters=3, s_true=s)
+    it = out["iters"][0]
+    assert it >= 1 and np.array_equal(out["xhat"][0, :N], s[0])
+    assert (out["trace"][0, it:] == N * p).all()
+    # x^(0): uniform source priors clip to symbol 0 -> bits of s that are 0 are right
+    assert out["trace"][0, 0] == _correct_bits_by_hand(np.zeros(N, np.uint8), s[0], p)
+    flipped = (s ^ 3).astype(np.uint8)   # every bit of the truth inverted
+    out2 = oc.decode(hard, pi, max_iters=3, s_true=flipped)
+    assert (out2["trace"][0, it:] == 0).all()
