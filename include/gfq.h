@@ -75,6 +75,20 @@ typedef struct {
     int keep_messages; /* 1: keep the final q, r messages and all posteriors Q
                           in the workspace for gfq_export_messages (needs a
                           workspace sized with the same flag).                */
+    /* Optional instrumentation of the paper's Fig. 1, device
+     * pointers, both NULL to disable (gfq_decode and gfq_decode_evidence only;
+     * gfq_decode_host rejects them):
+     *   trace_truth uint8 [n_frames][N]: the true source symbols s;
+     *   trace       int32 [n_frames][max_iters+1] out: trace[f][t] = number of
+     *               source bits (N*p per frame, bits as in A2) of the estimate
+     *               x^(t) equal to s -- t = 0 the clipped priors, t >= 1 the
+     *               clipped pseudo-posterior after iteration t.
+     *               After a frame stops (early_exit) its estimate is frozen
+     *               and the count repeats up to max_iters.
+     * The count is taken on the device after every iteration (one extra
+     * kernel reading N bytes of estimates per frame). */
+    const unsigned char *trace_truth;
+    int *trace;
 } gfq_params;
 
 /* Thread-local description of the last error (never NULL). */
@@ -186,7 +200,7 @@ int gfq_decode_stats(const gfq_code *code, const void *workspace, size_t ws_byte
  * duration in ms (ms[k]) and the number of launches (launches[k]); NULL outputs
  * are skipped.  gfq_kernel_name(k) names kind k ("cn", "vn", "sus", ...) or
  * returns NULL for k out of range. */
-#define GFQ_NKERNELS 13
+#define GFQ_NKERNELS 14
 int gfq_profile_enable(int on);
 int gfq_profile_read(double *ms, long long *launches);
 const char *gfq_kernel_name(int kind);

@@ -25,17 +25,30 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
     lib = out or LIB
     if not force and not defines and not _stale():
         return LIB
-    objs = []
     tag = ("_" + os.path.basename(lib).replace(".so", "")) if out else ""
-    for src in SOURCES:
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
+    headers.append(os.path.join(HERE, "..", "include", "gfq.h"))
+    hdr_t = max(os.path.getmtime(h) for h in headers)
+
+    def compile_one(src):
         obj = os.path.join(CSRC, src.replace(".cu", tag + ".o"))
-        cmd = [NVCC, *FLAGS, *["-D" + d for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
+        path = os.path.join(CSRC, src)
+        if (not force and not defines and os.path.exists(obj)
+                and os.path.getmtime(obj) > max(os.path.getmtime(path), hdr_t)):
+            return obj, ""      # object newer than its source and every header
+        cmd = [NVCC, *FLAGS, *["-D" + d for d in defines], "-c", path, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError("nvcc failed for %s:\n%s" % (src, res.stderr[-8000:]))
-        if verbose:
-            print(res.stderr)
-        objs.append(obj)
+        return obj, res.stderr
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    objs = [o for o, _ in results]
+    if verbose:
+        for _, err in results:
+            print(err)
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib, *objs,
            "-Xcompiler", "-fPIC"]
     res = subprocess.run(cmd, capture_output=True, text=True)

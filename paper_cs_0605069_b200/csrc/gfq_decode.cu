@@ -86,6 +86,10 @@ static int check_params(const gfq_code *c, const gfq_params *prm, bool need_chan
       if (std::fabs(s - 1.0) > 1e-6) { set_error("markov_T row is not stochastic"); return GFQ_EINVAL; }
     }
   }
+  if ((prm->trace == nullptr) != (prm->trace_truth == nullptr)) {
+    set_error("trace and trace_truth must both be set or both be NULL");
+    return GFQ_EINVAL;
+  }
   if (prm->src_pi0) {
     double s = 0.0;
     for (int a = 0; a < q; ++a) {
@@ -116,9 +120,10 @@ static T *at(void *ws, size_t off) {
 
 // ---------------------------------------------------------------- profiling
 enum Kind { K_FRONTEND, K_SYNDROME, K_INIT_MSGS, K_INIT_STATE, K_CN, K_VN, K_SUS, K_TEST, K_FINALIZE,
-            K_CAPTURE, K_COMPACT, K_CLIP, K_OTHER, K_N };
+            K_CAPTURE, K_COMPACT, K_CLIP, K_OTHER, K_TRACE, K_N };
 static const char *kKindNames[K_N] = {"frontend", "syndrome", "init_msgs", "init_state", "cn", "vn",
-                                      "sus", "test", "finalize", "capture", "compact", "clip", "other"};
+                                      "sus", "test", "finalize", "capture", "compact", "clip", "other",
+                                      "trace"};
 static_assert(K_N == GFQ_NKERNELS, "kernel kinds");
 
 struct Profiler {
@@ -214,6 +219,13 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
   if (ce == cudaSuccess) ce = cudaMemsetAsync(at<unsigned long long>(ws, L.stats), 0, 4 * sizeof(unsigned long long), st);
   if (ce != cudaSuccess) return cuda_fail(ce, "upload decoder constants");
 
+  const bool tracing = prm->trace != nullptr;
+  const int tlen = prm->max_iters + 1;
+  if (tracing) {
+    ce = cudaMemsetAsync(prm->trace, 0xff, sizeof(int) * (size_t)F * tlen, st);
+    if (ce != cudaSuccess) return cuda_fail(ce, "clear trace");
+  }
+
   LagRing &ring = lag_ring();
   unsigned long long launches = 0;
   int rc = GFQ_OK;
@@ -270,8 +282,12 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
     RUN(K_SYNDROME, launch_syndrome(a, st));
     RUN(K_INIT_MSGS, launch_init_msgs(a, st));
     RUN(K_INIT_STATE, launch_init_state(a, st));
-    if (prm->max_iters == 0) {
-      RUN(K_CLIP, launch_clip_priors(a, st));
+    if (prm->max_iters == 0 || tracing) {
+      // x^(0): the clipped priors; no posterior snapshot is written
+      WaveArgs a0 = a;
+      a0.qs_new = nullptr;
+      RUN(K_CLIP, launch_clip_priors(a0, st));
+      if (tracing) RUN(K_TRACE, launch_trace(a, prm->trace_truth, prm->trace, 0, tlen, st));
     }
     int t_done = 0;
     for (int t = 1; t <= prm->max_iters; ++t) {
@@ -294,6 +310,7 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
           if (n > 0) RUN(K_SUS, launch_sus_level(a, lb, n, st));
         }
       }
+      if (tracing) RUN(K_TRACE, launch_trace(a, prm->trace_truth, prm->trace, t, tlen, st));
       RUN(K_TEST, launch_test(a, st));
       RUN(K_FINALIZE, launch_finalize(a, 0, st));
       RUN(K_CAPTURE, launch_capture(a, out, Lout, 0, st));
@@ -313,6 +330,7 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
     ce = cudaMemcpyAsync(iters_out + (size_t)fb0 * 32, a.iters, sizeof(int) * nvalid, cudaMemcpyDeviceToDevice, st);
     if (ce != cudaSuccess) return cuda_fail(ce, "copy iters");
   }
+  if (tracing) RUN(K_TRACE, launch_trace_fill(prm->trace, F, tlen, st));
   RUN(K_OTHER, launch_set_u64(at<unsigned long long>(ws, L.stats) + 3, launches + 1, st));
 #undef RUN
   return GFQ_OK;
@@ -365,6 +383,7 @@ extern "C" int gfq_decode_host(const gfq_code *c, int n_frames, const void *obs_
   if (n_frames < 0) { set_error("n_frames < 0"); return GFQ_EINVAL; }
   if (n_frames == 0) return GFQ_OK;
   if (!obs_host || !s_hat_host || !iters_host || !ws) { set_error("NULL buffer"); return GFQ_EINVAL; }
+  if (prm->trace) { set_error("gfq_decode_host does not take trace buffers (device pointers)"); return GFQ_EINVAL; }
   const size_t ob = al256(obs_bytes(c, n_frames, prm));
   const size_t sb = al256((size_t)n_frames * c->N);
   const size_t ib = al256((size_t)n_frames * sizeof(int));

@@ -140,5 +140,7 @@ int launch_compact(const WaveArgs &a, cudaStream_t s);
 int launch_clip_priors(const WaveArgs &a, cudaStream_t s);
 int launch_export(const WaveArgs &a, float *q_out, float *r_out, float *Q_out, cudaStream_t s);
 int launch_set_u64(unsigned long long *p, unsigned long long v, cudaStream_t s);
+int launch_trace(const WaveArgs &a, const unsigned char *truth, int *trace, int t, int tlen, cudaStream_t s);
+int launch_trace_fill(int *trace, int n_frames, int tlen, cudaStream_t s);
 
 }  // namespace gfq

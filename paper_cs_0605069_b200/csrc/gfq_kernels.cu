@@ -251,6 +251,57 @@ __global__ void k_compact(WaveArgs a, unsigned int *host_count) {
 
 __global__ void k_set_u64(unsigned long long *p, unsigned long long v) { *p = v; }
 
+// ============================================================== Fig. 1 instrumentation
+// trace[f][t] = number of source bits of the current estimate x^(t) equal to
+// the true source s ("percentage of correct bits", times N*p/100).
+// One CTA per active 32-frame block; warp w takes 32-symbol tiles of the
+// source range; the truth tile [32 frames][32 symbols] is read row-wise
+// (coalesced) and transposed through shared memory so that lane = frame.
+__global__ void k_trace(WaveArgs a, const unsigned char *truth, int *trace, int t, int tlen) {
+  __shared__ unsigned char tile[8][32][33];
+  __shared__ int part[8][32];
+  const int fbi = blockIdx.x;
+  if (fbi >= *a.nactive) return;
+  const int fb = a.list[fbi];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int N = a.c.N, p = a.c.p;
+  const unsigned mask = (1u << p) - 1u;
+  const long long f0 = (long long)(a.fb0 + fb) * 32;
+  int ok = 0;
+  for (int j0 = w * 32; j0 < N; j0 += 8 * 32) {
+    for (int r = 0; r < 32; ++r) {
+      const long long f = f0 + r;
+      const int j = j0 + lane;
+      tile[w][r][lane] = (f < a.n_frames && j < N) ? truth[f * N + j] : 0;
+    }
+    __syncwarp();
+    const int jn = min(32, N - j0);
+    for (int jj = 0; jj < jn; ++jj) {
+      const unsigned x = a.xhat[((size_t)fb * a.c.V + j0 + jj) * 32 + lane];
+      ok += p - __popc((x ^ tile[w][lane][jj]) & mask);
+    }
+    __syncwarp();
+  }
+  part[w][lane] = ok;
+  __syncthreads();
+  if (w == 0) {
+    int s = 0;
+    for (int k = 0; k < 8; ++k) s += part[k][lane];
+    const long long f = f0 + lane;
+    if (f < a.n_frames) trace[f * tlen + t] = s;
+  }
+}
+
+// Frames that stopped early keep their estimate: forward-fill the entries of
+// iterations their block no longer ran (initialised to -1).
+__global__ void k_trace_fill(int *trace, int n_frames, int tlen) {
+  const long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n_frames) return;
+  int *tr = trace + f * tlen;
+  for (int t = 1; t < tlen; ++t)
+    if (tr[t] < 0) tr[t] = tr[t - 1];
+}
+
 // Export to [frame][canonical edge][q] / [frame][V][q] (debug and parity only).
 __global__ void k_export(WaveArgs a, const float *src, float *dst, int items, const int *map, float scale) {
   const int q = a.c.q;
@@ -333,6 +384,16 @@ int launch_export(const WaveArgs &a, float *q_out, float *r_out, float *Q_out, c
   if (r_out) k_export<<<grid, threads, 0, s>>>(a, a.rmsg, r_out, (int)a.c.E, nullptr, 1.0f / a.c.q);
   if (Q_out) k_export<<<grid, threads, 0, s>>>(a, a.qall, Q_out, a.c.V, nullptr, 1.0f);
   return check_launch("k_export");
+}
+
+int launch_trace(const WaveArgs &a, const unsigned char *truth, int *trace, int t, int tlen, cudaStream_t s) {
+  k_trace<<<a.nfb, 256, 0, s>>>(a, truth, trace, t, tlen);
+  return check_launch("k_trace");
+}
+
+int launch_trace_fill(int *trace, int n_frames, int tlen, cudaStream_t s) {
+  k_trace_fill<<<(n_frames + 255) / 256, 256, 0, s>>>(trace, n_frames, tlen);
+  return check_launch("k_trace_fill");
 }
 
 int launch_set_u64(unsigned long long *p, unsigned long long v, cudaStream_t s) {

@@ -25,7 +25,7 @@ EXPORTS = ["gfq_last_error", "gfq_version", "gfq_code_create", "gfq_code_destroy
            "gfq_workspace_bytes", "gfq_decode", "gfq_decode_evidence", "gfq_workspace_bytes_host",
            "gfq_decode_host", "gfq_export_messages", "gfq_decode_stats", "gfq_profile_enable",
            "gfq_profile_read", "gfq_kernel_name"]
-GFQ_NKERNELS = 13
+GFQ_NKERNELS = 14
 
 
 class GfqError(RuntimeError):
@@ -38,7 +38,8 @@ class gfq_params(ctypes.Structure):
     _fields_ = [("channel", ctypes.c_int), ("ch_param", ctypes.c_double),
                 ("schedule", ctypes.c_int), ("max_iters", ctypes.c_int),
                 ("early_exit", ctypes.c_int), ("markov_T", ctypes.c_void_p),
-                ("src_pi0", ctypes.c_void_p), ("keep_messages", ctypes.c_int)]
+                ("src_pi0", ctypes.c_void_p), ("keep_messages", ctypes.c_int),
+                ("trace_truth", ctypes.c_void_p), ("trace", ctypes.c_void_p)]
 
 
 _lib = None
@@ -109,14 +110,18 @@ class Params:
     """gfq_params plus the host arrays it points to (kept alive)."""
 
     def __init__(self, channel=GFQ_BSC, ch_param=0.0, schedule=GFQ_PUS, max_iters=100,
-                 early_exit=True, markov_T=None, src_pi0=None, keep_messages=False):
+                 early_exit=True, markov_T=None, src_pi0=None, keep_messages=False,
+                 trace_truth=None, trace=None):
+        """trace_truth / trace: CUDA tensors uint8 [F][N] and int32 [F][max_iters+1]
+        (Fig. 1 instrumentation, see include/gfq.h), or None."""
         self._T = None if markov_T is None else np.ascontiguousarray(markov_T, dtype=np.float64)
+        self._trace = (trace_truth, trace)
         self._pi0 = None if src_pi0 is None else np.ascontiguousarray(src_pi0, dtype=np.float64)
         self.c = gfq_params(int(channel), float(ch_param), int(schedule), int(max_iters),
                             int(bool(early_exit)),
                             None if self._T is None else self._T.ctypes.data,
                             None if self._pi0 is None else self._pi0.ctypes.data,
-                            int(bool(keep_messages)))
+                            int(bool(keep_messages)), _dptr(trace_truth), _dptr(trace))
 
     def ref(self):
         return ctypes.byref(self.c)

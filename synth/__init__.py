@@ -394,5 +394,24 @@ def stationary(T: np.ndarray, iters: int = 10000) -> np.ndarray:
     return pi / pi.sum()
 
 
+def markov_embed_binary(T2: np.ndarray, p: int) -> np.ndarray:
+    """Symbol-level transition matrix of a binary Markov chain read p bits per
+    GF(2^p) symbol, bit 0 first (reading A2): T[a][b] = T2[a_{p-1}][b_0] *
+    prod_{k>=1} T2[b_{k-1}][b_k].  The paper's GF(8) rows use the 2-state
+    source this way (an ambiguity of the paper)."""
+    q = 1 << p
+    T = np.zeros((q, q), dtype=np.float64)
+    for a in range(q):
+        prev = (a >> (p - 1)) & 1
+        for b in range(q):
+            v, last = 1.0, prev
+            for k in range(p):
+                bit = (b >> k) & 1
+                v *= T2[last, bit]
+                last = bit
+            T[a, b] = v
+    return T
+
+
 def markov_T_for(cfg: Config) -> Optional[np.ndarray]:
     return markov_uniform_jump(cfg.q, cfg.stay) if cfg.source == "markov" else None

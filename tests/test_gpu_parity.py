@@ -276,3 +276,51 @@ def test_markov_sus_pus_full_c2_sampled_decisions(gfq):
         match, _ = _decision_match(s_hat, iters, ref["xhat"][:, :code.N], ref["iters"])
         assert int((~match).sum()) == 0
         assert (iters > 3).mean() > 0.5   # the noisier point really iterates
+
+
+TRACE_CASES = [("C1", 64, 0, False), ("C2", 96, 0, False), ("C3", 40, 4, True), ("C4", 40, 0, False)]
+
+
+@pytest.mark.parametrize("schedule", [0, 1], ids=["PUS", "SUS"])
+@pytest.mark.parametrize("name,nframes,point,fixed", TRACE_CASES)
+def test_trace_fig1(gfq, name, nframes, point, fixed, schedule):
+    """Fig. 1 instrumentation: the correct-source-bit count of the
+    estimate after every iteration, taken on the device, equals the oracle's
+    count (integers; the estimates themselves are argmaxes of fp32 vs fp64
+    posteriors, so equality is required on >= 99.9 % of frames, reading A18)."""
+    cfg, code, fr = _setup(name, nframes, point)
+    T = synth.markov_T_for(cfg)
+    gcode = gfq.Code.from_synth(code)
+    tmax = 25 if fixed else cfg.max_iters
+    truth = torch.as_tensor(fr.s).cuda()
+    trace = torch.zeros((fr.F, tmax + 1), dtype=torch.int32, device="cuda")
+    prm = gfq.Params(_channel(gfq, fr), fr.ch_param, schedule, tmax, early_exit=not fixed, markov_T=T,
+                     trace_truth=truth, trace=trace)
+    s_hat, iters, ws = gfq.gfq_decode(gcode, torch.as_tensor(fr.obs).cuda(), prm)
+    torch.cuda.synchronize()
+    oc = oracle.OCode.from_synth(code)
+    hard, pi = oracle.frontend(fr.channel, fr.ch_param, fr.obs)
+    ref = oc.decode(hard, pi, schedule=schedule, max_iters=tmax, fixed=fixed, T=T, s_true=fr.s)
+    tg = trace.cpu().numpy()
+    same = (tg == ref["trace"]).all(axis=1)
+    print(name, "trace mismatching frames", int((~same).sum()), "of", fr.F)
+    assert (tg >= 0).all() and (tg <= code.N * code.p).all()
+    assert int((~same).sum()) <= int(np.floor(0.001 * fr.F))
+    # the count of the final estimate is the count of the returned s_hat
+    sh = s_hat.cpu().numpy()
+    bits = lambda a: np.unpackbits(a[..., None], axis=-1, bitorder="little")[..., :code.p]
+    final = (bits(sh) == bits(fr.s)).sum(axis=(1, 2))
+    conv = iters.cpu().numpy() > 0
+    if not fixed:
+        assert np.array_equal(tg[:, -1], final)
+    else:
+        assert np.array_equal(tg[~conv, -1], final[~conv])
+
+
+def test_trace_requires_both_buffers(gfq):
+    cfg, code, fr = _setup("C1", 4)
+    gcode = gfq.Code.from_synth(code)
+    trace = torch.zeros((fr.F, 6), dtype=torch.int32, device="cuda")
+    prm = gfq.Params(_channel(gfq, fr), fr.ch_param, 0, 5, trace=trace)
+    with pytest.raises(gfq.GfqError):
+        gfq.gfq_decode(gcode, torch.as_tensor(fr.obs).cuda(), prm)

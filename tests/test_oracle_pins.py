@@ -606,3 +606,20 @@ def test_trace_point_cases():
     flipped = (s ^ 3).astype(np.uint8)   # every bit of the truth inverted
     out2 = oc.decode(hard, pi, max_iters=3, s_true=flipped)
     assert (out2["trace"][0, it:] == 0).all()
+
+
+def test_embedded_binary_chain_matches_bit_chain():
+    """The GF(8) symbol chain built from the 2S matrix gives the same
+    law as the binary chain read 3 bits at a time: brute force over all bit
+    strings of two symbols."""
+    T2 = synth.MARKOV_2S
+    T8 = synth.markov_embed_binary(T2, 3)
+    assert np.allclose(T8.sum(axis=1), 1.0, atol=1e-12)
+    for a in range(8):
+        for b in range(8):
+            bits = [(a >> k) & 1 for k in range(3)] + [(b >> k) & 1 for k in range(3)]
+            pr_b_given_a = np.prod([T2[bits[k - 1], bits[k]] for k in range(3, 6)])
+            assert math.isclose(T8[a, b], pr_b_given_a, rel_tol=1e-12)
+    # symmetric 2S: uniform bits, so the symbol law is 1/2 * prod of the in-symbol transitions
+    pi = [0.5 * T2[b & 1, (b >> 1) & 1] * T2[(b >> 1) & 1, (b >> 2) & 1] for b in range(8)]
+    assert np.allclose(synth.stationary(T8), pi, atol=1e-12)
