@@ -699,10 +699,13 @@ struct PPof {
 // ============================================================== shared-memory layout
 // [mbarriers][G*S headers of kHdr][pad][G*S payload slots, each a multiple of
 // PAL = q*128 bytes and PAL-aligned in the shared window][G scratch areas]
-template <int Q, int S, int G, size_t PAY, size_t SCR, size_t XTRA = 0, size_t TSMB = 0>
+// ALIGN: payload slots aligned to q*128 bytes (needed by the XOR row addressing
+// of perm_addrs, i.e. the check-node kernel); the variable-node and SUS kernels
+// address rows by addition and only need 128-byte alignment.
+template <int Q, int S, int G, size_t PAY, size_t SCR, size_t XTRA = 0, size_t TSMB = 0, bool ALIGN = true>
 struct Shape {
   static constexpr size_t TSM_B = ((TSMB + 127) / 128) * 128;
-  static constexpr size_t PAL = (size_t)Q * 128;
+  static constexpr size_t PAL = ALIGN ? (size_t)Q * 128 : 128;
   static constexpr size_t PAYA = ((PAY + PAL - 1) / PAL) * PAL;
   static constexpr size_t BARS_B = ((16 * S * G + 127) / 128) * 128;
   static constexpr size_t HDR_B = (size_t)G * S * kHdr;
@@ -1008,7 +1011,7 @@ struct VNShape {
   static constexpr int XR = Extra<Q, MARKOV>::rows;
   static constexpr size_t PAY = (size_t)DVMAX * Q * 128;
   static constexpr size_t SCR = ((size_t)(DVMAX + 2) * T * 32 + (size_t)(DVMAX + 2) * 32 + T * 32) * 8;
-  using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, MARKOV ? (size_t)2 * Q * Q * 4 : 0>;
+  using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, MARKOV ? (size_t)2 * Q * Q * 4 : 0, false>;
   static constexpr size_t SMEM = Sh::SMEM;
   static constexpr int THREADS = (G * T + (PWof<T>::v ? 1 : 0)) * 32;
 };
@@ -1150,7 +1153,11 @@ struct SUSShape {
   static constexpr size_t XR_D = XP_D > RED_D ? XP_D : RED_D;
   static constexpr size_t RSM_F = (size_t)DVMAX * Q * 32;
   static constexpr size_t SCR = XR_D * 8 + RSM_F * 4;
-  using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, MARKOV ? (size_t)2 * Q * Q * 4 : 0>;
+  // phased layout switches (sus_check_phased); the variable-node reduction
+  // scratch then lives in the stage payload of the column's last unit
+  static constexpr bool PHASED = PP && T > 1 && DMAX <= 4;
+  static_assert(!PHASED || RED_D * 8 <= PAY, "reduction scratch must fit a stage payload");
+  using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, MARKOV ? (size_t)2 * Q * Q * 4 : 0, false>;
   static constexpr size_t SMEM = Sh::SMEM;
   static constexpr int THREADS = (G * T + (PWof<T>::v ? 1 : 0)) * 32;
 };
@@ -1261,10 +1268,124 @@ __device__ __forceinline__ void sus_check(const WaveArgs &a, const unsigned char
   }
 }
 
+// Phased variant of sus_check for large fields (q >= 32, check degree <= 4):
+// the d-1 <= 3 forward layout switches take one barrier for the first two
+// messages (group scratch xp, slots 0 and 1) and one more for a third (the
+// task's own stage payload, free once every warp has passed the first
+// barrier, i.e. has read its inputs); the inverse switch writes the
+// accumulator over the buffer this warp read last, at the positions it read
+// (layout B): no other warp touches those positions between the barriers, so
+// no extra barrier is needed, and the positions read afterwards (layout A)
+// are exactly the ones this warp writes first in the next task.  Barriers
+// per unit: 2 (d = 3) or 3 (d = 4) instead of d.
+template <int Q, int KR, int DO, typename RF>
+__device__ __forceinline__ void sus_check_phased(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_u32,
+                                                 double *stage_x, uint64_t *empty, bool last, double *xp,
+                                                 float *rsm, const unsigned short *rowtab, int g, int c, int lane,
+                                                 bool frozen, RF &&refill) {
+  using C = QC<Q, KR>;
+  constexpr int T = C::T, LKR = C::LKR, LT = C::LT;
+  static_assert(T > 1 && DO <= 3, "phased SUS check: large fields, degree <= 4");
+  const TaskInfo ti = *(const TaskInfo *)hdr;
+  const SusDesc *sd = (const SusDesc *)(hdr + 128);
+  const int z = hdr[256 + lane];
+  const unsigned long long pke = sd->perm_e;
+  const int s = ti.s;
+  double acc[KR];
+  if constexpr (DO == 0) {
+    // degree-1 check: the convolution of no messages is the point mass at 0, so
+    // r(a) = [h_e a = z] (times q, the dropped 1/q of the inverse transform)
+    if (!last) {
+      release_stage(empty, lane);
+      refill();
+    }
+    const int az = rowtab[(size_t)(pke & 0xff) * Q + z] >> 7;  // h_e^-1 z
+#pragma unroll
+    for (int k = 0; k < KR; ++k) acc[k] = (c * KR + k == az) ? (double)Q : 0.0;
+    float *rs = rsm + (size_t)s * Q * 32 + lane + c * KR * 32;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) rs[k * 32] = (float)acc[k];
+    if (a.rmsg != nullptr && !frozen) {
+      float *rdst = a.rmsg + ((size_t)ti.fb * a.c.E + ti.e0 + s) * Q * 32 + lane + c * KR * 32;
+#pragma unroll
+      for (int k = 0; k < KR; ++k) rdst[k * 32] = (float)acc[k];
+    }
+    return;
+  } else {
+    double v[DO][KR];
+#pragma unroll
+    for (int t = 0; t < DO; ++t) {
+      uint32_t ad[KR];
+      tab_addrs<Q, KR>(pay_u32 + (uint32_t)(t * Q * 128 + lane * 4), rowtab, sd->perm_o[t], c, ad);
+#pragma unroll
+      for (int k = 0; k < KR; ++k) v[t][k] = (double)lds_f32(ad[k]);
+    }
+    if (DO <= 2 && !last) {
+      release_stage(empty, lane);
+      refill();
+    }
+#pragma unroll
+    for (int t = 0; t < DO; ++t) wht_bits<KR, 0, LKR>(v[t]);
+    constexpr int D1 = DO < 2 ? DO : 2;
+#pragma unroll
+    for (int t = 0; t < D1; ++t)
+#pragma unroll
+      for (int k = 0; k < KR; ++k) xp[((size_t)t * Q + idxA<Q, KR>(c, k)) * 32 + lane] = v[t][k];
+    group_bar<T>(g);
+#pragma unroll
+    for (int t = 0; t < D1; ++t)
+#pragma unroll
+      for (int k = 0; k < KR; ++k) v[t][k] = xp[((size_t)t * Q + idxB<Q, KR>(c, k)) * 32 + lane];
+    double *Z = xp;
+    if constexpr (DO == 3) {
+#pragma unroll
+      for (int k = 0; k < KR; ++k) stage_x[idxA<Q, KR>(c, k) * 32 + lane] = v[2][k];
+      group_bar<T>(g);
+#pragma unroll
+      for (int k = 0; k < KR; ++k) v[2][k] = stage_x[idxB<Q, KR>(c, k) * 32 + lane];
+      Z = stage_x;
+    }
+#pragma unroll
+    for (int t = 0; t < DO; ++t) wht_bits<KR, LKR - LT, LKR>(v[t]);
+    uint32_t sm[KR];
+    sign_masks<KR, T>(z, c, sm);
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      double x = v[0][k];
+#pragma unroll
+      for (int t = 1; t < DO; ++t) x *= v[t][k];
+      acc[k] = flip(x, sm[k]);
+    }
+    wht_bits<KR, LKR - LT, LKR>(acc);
+#pragma unroll
+    for (int k = 0; k < KR; ++k) Z[idxB<Q, KR>(c, k) * 32 + lane] = acc[k];
+    group_bar<T>(g);
+#pragma unroll
+    for (int k = 0; k < KR; ++k) acc[k] = Z[idxA<Q, KR>(c, k) * 32 + lane];
+    if (DO == 3 && !last) {
+      release_stage(empty, lane);  // the stage served as a transpose buffer
+      refill();
+    }
+    wht_bits<KR, 0, LKR>(acc);
+    uint32_t ad[KR];
+    tab_addrs<Q, KR>(0u, rowtab, pke, c, ad);  // ad[k] = (h_e^-1 y) * 128: a = h_e^-1 y
+    unsigned char *rs = (unsigned char *)(rsm + (size_t)s * Q * 32 + lane);
+#pragma unroll
+    for (int k = 0; k < KR; ++k) *(float *)(rs + ad[k]) = fmaxf((float)acc[k], 0.0f);
+    if (a.rmsg != nullptr) {  // keep_messages only (export): warp-uniform branch
+      if (!frozen) {
+        unsigned char *rdst = (unsigned char *)(a.rmsg + ((size_t)ti.fb * a.c.E + ti.e0 + s) * Q * 32 + lane);
+#pragma unroll
+        for (int k = 0; k < KR; ++k) *(float *)(rdst + ad[k]) = fmaxf((float)acc[k], 0.0f);
+      }
+    }
+  }
+}
+
 template <int Q, int KR, int DV, int DVMAX, bool MARKOV, typename RF>
 __device__ __forceinline__ void sus_vn(const WaveArgs &a, const unsigned char *hdr, const unsigned char *xtra,
                                        const float *Tsm, uint64_t *empty, const float *rsm, double *red, int g,
-                                       int c, int lane, bool frozen, RF &&refill) {
+                                       int c, int lane, bool frozen, bool late_release, RF &&refill) {
   const TaskInfo ti = *(const TaskInfo *)hdr;
   const VarDesc *vd = (const VarDesc *)(hdr + 192);
   int qdst[DV > 0 ? DV : 1];
@@ -1277,9 +1398,15 @@ __device__ __forceinline__ void sus_vn(const WaveArgs &a, const unsigned char *h
   }
   double pr[KR];
   prior_from<Q, KR, MARKOV>(a, ti.item, c, lane, (const float *)xtra, Tsm, pr);
-  release_stage(empty, lane);
-  refill();
+  if (!late_release) {
+    release_stage(empty, lane);
+    refill();
+  }
   vn_core<Q, KR, DV, MARKOV>(a, ti.fb, ti.item, qdst, r, pr, red, g, c, lane, frozen);
+  if (late_release) {  // red lives in the stage payload
+    release_stage(empty, lane);
+    refill();
+  }
 }
 
 // For every column j of the level (SUS step 1): r_ij for each
@@ -1371,7 +1498,19 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       nunits = dv > 0 ? dv : 1;
       const bool last = (s == nunits - 1);
       const bool frozen = a.early_exit && ((const int *)(hdr + 384))[lane] != 0;
-      if (dv > 0) {
+      double *stage_x = (double *)(sp.pay + (size_t)k * Sh::PAYA);
+      if constexpr (SS::PHASED) {
+        if (dv > 0) {
+#define SP(n) sus_check_phased<Q, KR, n>(a, hdr, pay_u32, stage_x, empty, last, xp, rsm, a.c.rowtab, g, c, lane, frozen, refill)
+          switch (d - 1) {
+            case 0: SP(0); break;
+            case 1: SP(1); break;
+            case 2: SP(2); break;
+            default: SP(3); break;
+          }
+#undef SP
+        }
+      } else if (dv > 0) {
 #define SC(n) sus_check<Q, KR, n, DMAX>(a, hdr, pay_u32, empty, !last, xp, m, rsm, g, c, lane, frozen, refill)
         switch (d - 1) {
           case 0: SC(0); break;
@@ -1396,7 +1535,7 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       if (last) {
         // vertical update of column j from the fresh r's (SUS step 2)
         group_bar<T>(g);  // rsm complete, transpose buffers free for the reduction
-#define SV(n) sus_vn<Q, KR, n, DVMAX, MARKOV>(a, hdr, xtra, sp.tsm, empty, rsm, red, g, c, lane, frozen, refill)
+#define SV(n) sus_vn<Q, KR, n, DVMAX, MARKOV>(a, hdr, xtra, sp.tsm, empty, rsm, SS::PHASED ? stage_x : red, g, c, lane, frozen, SS::PHASED, refill)
         switch (dv) {
           case 0: SV(0); break;
           case 1: SV(1); break;
@@ -1417,13 +1556,14 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
             break;
         }
 #undef SV
-        if constexpr (SS::PP && SS::RED_D <= (size_t)Q * 32) m = 1;  // next transpose avoids red (buffer 0)
+        if constexpr (!SS::PHASED && SS::PP && SS::RED_D <= (size_t)Q * 32) m = 1;  // next transpose avoids red (buffer 0)
       }
       // Ping-pong transposes need no barrier between units (rsm slots are
       // distinct; the next rsm write follows a transpose barrier), and after
       // the variable update the next transpose writes buffer 1 while the
       // reduction scratch lives in buffer 0.  Bulk mode reuses its buffers.
-      if constexpr (!SS::PP || SS::RED_D > (size_t)Q * 32) group_bar<T>(g);
+      // Phased mode needs none either (see sus_check_phased; red is in the stage).
+      if constexpr (!SS::PHASED && (!SS::PP || SS::RED_D > (size_t)Q * 32)) group_bar<T>(g);
     }
   }
 }

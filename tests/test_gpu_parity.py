@@ -324,3 +324,57 @@ def test_trace_requires_both_buffers(gfq):
     prm = gfq.Params(_channel(gfq, fr), fr.ch_param, 0, 5, trace=trace)
     with pytest.raises(gfq.GfqError):
         gfq.gfq_decode(gcode, torch.as_tensor(fr.obs).cuda(), prm)
+
+
+def _low_degree_code(p, N, M, seed):
+    """Check degrees 1..4 (including degree-1 and degree-2 checks) and variable
+    degrees 1..3: the q >= 32 SUS path with phased layout switches takes every
+    branch (d - 1 = 0, 1, 2, 3)."""
+    rng = np.random.default_rng(seed)
+    q = 1 << p
+    V = N + M
+    cap = rng.integers(1, 5, M)           # check degrees 1..4
+    cap[:4] = [1, 2, 3, 4]
+    vdeg = np.zeros(V, int)
+    rows, cols = [], []
+    for i in range(M):
+        # variables of lowest degree first (every variable gets an edge), at most 3 each
+        order = np.lexsort((rng.random(V), vdeg))
+        pick = [j for j in order if vdeg[j] < 3][:cap[i]]
+        for j in pick:
+            rows.append(i); cols.append(int(j)); vdeg[j] += 1
+    rows = np.array(rows, np.int32); cols = np.array(cols, np.int32)
+    o = np.lexsort((cols, rows))
+    rows, cols = rows[o], cols[o]
+    vals = rng.integers(1, q, len(rows)).astype(np.uint8)
+    a = cols < N
+    A = (rows[a], cols[a], vals[a])
+    B = (rows[~a], cols[~a] - N, vals[~a])
+    return rows, cols, vals, A, B
+
+
+@pytest.mark.parametrize("p", [5, 6])
+def test_low_degree_code_large_field_message_parity(gfq, p):
+    N, M = 30, 50
+    for seed in range(300, 400):
+        rows, cols, vals, A, B = _low_degree_code(p, N, M, seed)
+        deg = np.bincount(rows, minlength=M)
+        vdeg = np.bincount(cols, minlength=N + M)
+        if deg.min() >= 1 and deg.max() <= 4 and vdeg.max() <= 3 and {1, 2, 3, 4} <= set(deg.tolist()):
+            break
+    assert {1, 2, 3, 4} <= set(deg.tolist()) and vdeg.max() <= 3
+    gcode = gfq.Code(p, synth.PRIM_POLY[p], N, M, *A, *B)
+    oc = oracle.OCode(p, synth.PRIM_POLY[p], N, M, rows, cols, vals)
+    rng = np.random.default_rng(p + 7)
+    F = 45                                 # two blocks, ragged
+    hard = rng.integers(0, 2, (F, M * p)).astype(np.uint8)
+    pi = rng.uniform(0.02, 0.3, (F, M * p)).astype(np.float32)
+    for schedule in (0, 1):
+        prm = gfq.Params(schedule=schedule, max_iters=4, early_exit=False, keep_messages=True)
+        x, it, ws = gfq.gfq_decode_evidence(gcode, torch.as_tensor(hard).cuda(), torch.as_tensor(pi).cuda(), prm)
+        qg, rg, Qg = gfq.gfq_export_messages(gcode, F, ws, prm)
+        ref = oc.decode(hard, pi.astype(np.float64), schedule=schedule, max_iters=4, fixed=True, keep_messages=True)
+        assert float(np.max(np.abs(qg.cpu().numpy() - ref["q"]))) <= MSG_TOL
+        assert float(np.max(np.abs(rg.cpu().numpy() - ref["r"]))) <= MSG_TOL
+        assert float(np.max(np.abs(Qg.cpu().numpy() - ref["Q"]))) <= MSG_TOL
+        assert np.array_equal(it.cpu().numpy(), ref["iters"])
