@@ -57,7 +57,7 @@ struct QC {
 
 // entries per thread by field size and kernel (tuning knobs)
 #ifndef GFQ_KR_CN16
-#define GFQ_KR_CN16 8
+#define GFQ_KR_CN16 16
 #endif
 #ifndef GFQ_KR_VN16
 #define GFQ_KR_VN16 8
@@ -484,7 +484,9 @@ __device__ __forceinline__ void prior_from(const WaveArgs &a, int j, int c, int 
 // r[s][k] holds r of check slot s at a = c*KR + k (any positive scale: every
 // output is normalised); pr the prior; qdst[s] the check-major id of the edge
 // of slot s.  red: group scratch of (DV+2)*T*32 doubles (T > 1).
-template <int Q, int KR, int DV, bool MARKOV>
+// ONEBAR (T <= 4, red private to the task): one barrier, every warp sums the
+// T partials itself (the two-step reduction needs two).
+template <int Q, int KR, int DV, bool MARKOV, bool ONEBAR = false>
 __device__ __forceinline__ void vn_core(const WaveArgs &a, int fb, int j, const int *qdst, double (&r)[DV > 0 ? DV : 1][KR],
                                         const double (&pr)[KR], double *red, int g, int c, int lane, bool frozen) {
   constexpr int T = Q / KR;
@@ -538,7 +540,22 @@ __device__ __forceinline__ void vn_core(const WaveArgs &a, int fb, int j, const 
     sums[DV] += tot[k];
     if (k > 0) mx = fmax(mx, tot[k]);
   }
-  if constexpr (T > 1) {
+  if constexpr (T > 1 && ONEBAR) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) red[((size_t)s * T + c) * 32 + lane] = sums[s];
+    red[((size_t)NS * T + c) * 32 + lane] = mx;
+    group_bar<T>(g);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      double v = red[((size_t)s * T) * 32 + lane];
+#pragma unroll
+      for (int cc = 1; cc < T; ++cc) v += red[((size_t)s * T + cc) * 32 + lane];
+      sums[s] = v;
+    }
+    mx = red[((size_t)NS * T) * 32 + lane];
+#pragma unroll
+    for (int cc = 1; cc < T; ++cc) mx = fmax(mx, red[((size_t)NS * T + cc) * 32 + lane]);
+  } else if constexpr (T > 1) {
     // two-step cross-warp reduction: partials -> warp v reduces value v -> totals
 #pragma unroll
     for (int s = 0; s < NS; ++s) red[((size_t)s * T + c) * 32 + lane] = sums[s];
@@ -1010,7 +1027,9 @@ struct VNShape {
   static constexpr int T = Q / KR;
   static constexpr int XR = Extra<Q, MARKOV>::rows;
   static constexpr size_t PAY = (size_t)DVMAX * Q * 128;
-  static constexpr size_t SCR = ((size_t)(DVMAX + 2) * T * 32 + (size_t)(DVMAX + 2) * 32 + T * 32) * 8;
+  static constexpr bool ONEBAR = T > 1 && T <= 4;  // one-barrier reduction, red double-buffered
+  static constexpr size_t RED_B = ((size_t)(DVMAX + 2) * T * 32 + (size_t)(DVMAX + 2) * 32 + T * 32) * 8;
+  static constexpr size_t SCR = RED_B * (ONEBAR ? 2 : 1);
   using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, MARKOV ? (size_t)2 * Q * Q * 4 : 0, false>;
   static constexpr size_t SMEM = Sh::SMEM;
   static constexpr int THREADS = (G * T + (PWof<T>::v ? 1 : 0)) * 32;
@@ -1051,7 +1070,7 @@ __device__ __forceinline__ void vn_task(const WaveArgs &a, const unsigned char *
   prior_from<Q, KR, MARKOV>(a, ti.item, c, lane, (const float *)xtra, Tsm, pr);
   release_stage(empty, lane);
   refill();
-  vn_core<Q, KR, DV, MARKOV>(a, ti.fb, ti.item, qdst, r, pr, red, g, c, lane, frozen);
+  vn_core<Q, KR, DV, MARKOV, (Q / KR > 1 && Q / KR <= 4)>(a, ti.fb, ti.item, qdst, r, pr, red, g, c, lane, frozen);
 }
 
 template <int Q, int KR, int DVMAX, bool MARKOV, int S, int G>
@@ -1114,7 +1133,8 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
     };
     mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
     const int dv = ((const TaskInfo *)hdr)->deg;
-#define VT(n) vn_task<Q, KR, n, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, red, g, c, lane, refill)
+    double *redt = VS::ONEBAR ? red + (size_t)(rr & 1) * (VS::RED_B / 8) : red;
+#define VT(n) vn_task<Q, KR, n, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, redt, g, c, lane, refill)
     switch (dv) {
       case 0: VT(0); break;
       case 1: VT(1); break;
@@ -1148,14 +1168,14 @@ struct SUSShape {
   static constexpr size_t PAY = (size_t)(DMAX - 1) * Q * 128;
   // transpose buffers (bulk: DMAX-1 forward + 1 accumulator; ping-pong: 2);
   // the variable-node reduction scratch aliases them (used after the last transpose)
-  static constexpr size_t XP_D = T > 1 ? (size_t)(PP ? 2 : DMAX) * Q * 32 : 0;
+  static constexpr bool PHASED = T > 1 && DMAX <= 4;  // sus_check_phased
+  static constexpr size_t XP_D = T > 1 ? (size_t)((PP || PHASED) ? 2 : DMAX) * Q * 32 : 0;
   static constexpr size_t RED_D = (size_t)(DVMAX + 2) * T * 32 + (size_t)(DVMAX + 2) * 32 + T * 32;
   static constexpr size_t XR_D = XP_D > RED_D ? XP_D : RED_D;
   static constexpr size_t RSM_F = (size_t)DVMAX * Q * 32;
   static constexpr size_t SCR = XR_D * 8 + RSM_F * 4;
-  // phased layout switches (sus_check_phased); the variable-node reduction
+  // phased layout switches (sus_check_phased): the variable-node reduction
   // scratch then lives in the stage payload of the column's last unit
-  static constexpr bool PHASED = PP && T > 1 && DMAX <= 4;
   static_assert(!PHASED || RED_D * 8 <= PAY, "reduction scratch must fit a stage payload");
   using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, MARKOV ? (size_t)2 * Q * Q * 4 : 0, false>;
   static constexpr size_t SMEM = Sh::SMEM;
@@ -1268,7 +1288,7 @@ __device__ __forceinline__ void sus_check(const WaveArgs &a, const unsigned char
   }
 }
 
-// Phased variant of sus_check for large fields (q >= 32, check degree <= 4):
+// Phased variant of sus_check for q >= 16 (T > 1), check degree <= 4:
 // the d-1 <= 3 forward layout switches take one barrier for the first two
 // messages (group scratch xp, slots 0 and 1) and one more for a third (the
 // task's own stage payload, free once every warp has passed the first
@@ -1277,7 +1297,7 @@ __device__ __forceinline__ void sus_check(const WaveArgs &a, const unsigned char
 // (layout B): no other warp touches those positions between the barriers, so
 // no extra barrier is needed, and the positions read afterwards (layout A)
 // are exactly the ones this warp writes first in the next task.  Barriers
-// per unit: 2 (d = 3) or 3 (d = 4) instead of d.
+// per unit: 2 (d = 3) or 3 (d = 4) instead of d (ping-pong) or 3 (bulk).
 template <int Q, int KR, int DO, typename RF>
 __device__ __forceinline__ void sus_check_phased(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_u32,
                                                  double *stage_x, uint64_t *empty, bool last, double *xp,
@@ -1285,7 +1305,7 @@ __device__ __forceinline__ void sus_check_phased(const WaveArgs &a, const unsign
                                                  bool frozen, RF &&refill) {
   using C = QC<Q, KR>;
   constexpr int T = C::T, LKR = C::LKR, LT = C::LT;
-  static_assert(T > 1 && DO <= 3, "phased SUS check: large fields, degree <= 4");
+  static_assert(T > 1 && DO <= 3, "phased SUS check: q >= 16, degree <= 4");
   const TaskInfo ti = *(const TaskInfo *)hdr;
   const SusDesc *sd = (const SusDesc *)(hdr + 128);
   const int z = hdr[256 + lane];
@@ -1382,7 +1402,7 @@ __device__ __forceinline__ void sus_check_phased(const WaveArgs &a, const unsign
   }
 }
 
-template <int Q, int KR, int DV, int DVMAX, bool MARKOV, typename RF>
+template <int Q, int KR, int DV, int DVMAX, bool MARKOV, bool ONEBAR, typename RF>
 __device__ __forceinline__ void sus_vn(const WaveArgs &a, const unsigned char *hdr, const unsigned char *xtra,
                                        const float *Tsm, uint64_t *empty, const float *rsm, double *red, int g,
                                        int c, int lane, bool frozen, bool late_release, RF &&refill) {
@@ -1402,7 +1422,7 @@ __device__ __forceinline__ void sus_vn(const WaveArgs &a, const unsigned char *h
     release_stage(empty, lane);
     refill();
   }
-  vn_core<Q, KR, DV, MARKOV>(a, ti.fb, ti.item, qdst, r, pr, red, g, c, lane, frozen);
+  vn_core<Q, KR, DV, MARKOV, ONEBAR>(a, ti.fb, ti.item, qdst, r, pr, red, g, c, lane, frozen);
   if (late_release) {  // red lives in the stage payload
     release_stage(empty, lane);
     refill();
@@ -1535,7 +1555,7 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       if (last) {
         // vertical update of column j from the fresh r's (SUS step 2)
         group_bar<T>(g);  // rsm complete, transpose buffers free for the reduction
-#define SV(n) sus_vn<Q, KR, n, DVMAX, MARKOV>(a, hdr, xtra, sp.tsm, empty, rsm, SS::PHASED ? stage_x : red, g, c, lane, frozen, SS::PHASED, refill)
+#define SV(n) sus_vn<Q, KR, n, DVMAX, MARKOV, SS::PHASED && (T <= 4)>(a, hdr, xtra, sp.tsm, empty, rsm, SS::PHASED ? stage_x : red, g, c, lane, frozen, SS::PHASED, refill)
         switch (dv) {
           case 0: SV(0); break;
           case 1: SV(1); break;
@@ -1582,11 +1602,15 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
   set_error("unsupported q"); \
   return GFQ_EUNSUPPORTED;
 
+// stages per group (q = 16: 2, so that more CTAs fit an SM; measured on C4)
 #ifndef GFQ_STAGES_CN
 #define GFQ_STAGES_CN 3
 #endif
 #ifndef GFQ_STAGES_VN
 #define GFQ_STAGES_VN 3
+#endif
+#ifndef GFQ_STAGES_Q16
+#define GFQ_STAGES_Q16 2
 #endif
 #ifndef GFQ_STAGES_SUS
 #define GFQ_STAGES_SUS 2
@@ -1607,7 +1631,7 @@ constexpr int stages_fit(int want) {
 template <int Q, int DM>
 static int cn_launch(const WaveArgs &a, cudaStream_t s) {
   constexpr int KR = KRof<Q, KCN>::v, T = Q / KR, G = Gof<T, KCN>::v;
-  constexpr int NS = stages_fit<CNShape<Q, KR, DM, 1, G>, CNShape<Q, KR, DM, 2, G>>(GFQ_STAGES_CN);
+  constexpr int NS = stages_fit<CNShape<Q, KR, DM, 1, G>, CNShape<Q, KR, DM, 2, G>>(Q == 16 ? GFQ_STAGES_Q16 : GFQ_STAGES_CN);
   using CS = CNShape<Q, KR, DM, NS, G>;
   if (CS::SMEM > 232448) return too_big("k_cn");
   auto k = k_cn<Q, KR, DM, NS, G>;
@@ -1624,7 +1648,7 @@ static int cn_q(const WaveArgs &a, cudaStream_t s) {
 template <int Q, int DV, bool MK>
 static int vn_launch(const WaveArgs &a, int clip, cudaStream_t s) {
   constexpr int KR = KRof<Q, KVN>::v, T = Q / KR, G = Gof<T, KVN>::v;
-  constexpr int NS = stages_fit<VNShape<Q, KR, DV, MK, 1, G>, VNShape<Q, KR, DV, MK, 2, G>>(GFQ_STAGES_VN);
+  constexpr int NS = stages_fit<VNShape<Q, KR, DV, MK, 1, G>, VNShape<Q, KR, DV, MK, 2, G>>(Q == 16 ? GFQ_STAGES_Q16 : GFQ_STAGES_VN);
   using VS = VNShape<Q, KR, DV, MK, NS, G>;
   if (VS::SMEM > 232448) return too_big("k_vn");
   auto k = k_vn<Q, KR, DV, MK, NS, G>;
