@@ -320,6 +320,24 @@ __device__ __forceinline__ void tab_addrs(uint32_t base, const unsigned short *r
   for (int k = 0; k < KR; ++k) ad[k] = base + ((k & 1) ? (w[k >> 1] >> 16) : (w[k >> 1] & 0xffffu));
 }
 
+// The same from a shared-memory copy of the table (rt = its shared address).
+template <int Q, int KR>
+__device__ __forceinline__ void tab_addrs_sm(uint32_t base, uint32_t rt, unsigned long long pk, int c,
+                                             uint32_t (&ad)[KR]) {
+  static_assert(KR == 2 || KR == 4 || KR == 8, "tab_addrs_sm: KR");
+  const uint32_t p = rt + (uint32_t)(((size_t)(pk & 0xff) * Q + c * KR) * 2);
+  uint32_t w[4];
+  if constexpr (KR == 8) {
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(p));
+  } else if constexpr (KR == 4) {
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(p));
+  } else {
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w[0]) : "r"(p));
+  }
+#pragma unroll
+  for (int k = 0; k < KR; ++k) ad[k] = base + ((k & 1) ? (w[k >> 1] >> 16) : (w[k >> 1] & 0xffffu));
+}
+
 // ============================================================== leave-one-out with the syndrome sign
 // out_s = sign * prod_{s' != s} u_s'   for exact degree D (sign folded in as an
 // XOR of the high word: the same sign multiplies every output at frequency w).
@@ -1177,7 +1195,12 @@ struct SUSShape {
   // phased layout switches (sus_check_phased): the variable-node reduction
   // scratch then lives in the stage payload of the column's last unit
   static_assert(!PHASED || RED_D * 8 <= PAY, "reduction scratch must fit a stage payload");
-  using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, MARKOV ? (size_t)2 * Q * Q * 4 : 0, false>;
+  // shared region: Markov T and T^T (fp32), then the row-offset table (u16 q x q)
+  // when it still fits (RTS; otherwise the table is read through L1)
+  static constexpr size_t TSM_F = MARKOV ? (size_t)2 * Q * Q : 0;
+  using Sh0 = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, TSM_F * 4, false>;
+  static constexpr bool RTS = Sh0::SMEM + (size_t)2 * Q * Q <= 232448;
+  using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, TSM_F * 4 + (RTS ? (size_t)2 * Q * Q : 0), false>;
   static constexpr size_t SMEM = Sh::SMEM;
   static constexpr int THREADS = (G * T + (PWof<T>::v ? 1 : 0)) * 32;
 };
@@ -1298,11 +1321,19 @@ __device__ __forceinline__ void sus_check(const WaveArgs &a, const unsigned char
 // no extra barrier is needed, and the positions read afterwards (layout A)
 // are exactly the ones this warp writes first in the next task.  Barriers
 // per unit: 2 (d = 3) or 3 (d = 4) instead of d (ping-pong) or 3 (bulk).
-template <int Q, int KR, int DO, typename RF>
+// Row offsets from the shared (RTS) or global copy of the per-field table.
+template <int Q, int KR, bool RTS>
+__device__ __forceinline__ void row_addrs(uint32_t base, uint32_t rt, const unsigned short *rowtab,
+                                          unsigned long long pk, int c, uint32_t (&ad)[KR]) {
+  if constexpr (RTS) tab_addrs_sm<Q, KR>(base, rt, pk, c, ad);
+  else tab_addrs<Q, KR>(base, rowtab, pk, c, ad);
+}
+
+template <int Q, int KR, int DO, bool RTS, typename RF>
 __device__ __forceinline__ void sus_check_phased(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_u32,
                                                  double *stage_x, uint64_t *empty, bool last, double *xp,
-                                                 float *rsm, const unsigned short *rowtab, int g, int c, int lane,
-                                                 bool frozen, RF &&refill) {
+                                                 float *rsm, uint32_t rt, const unsigned short *rowtab,
+                                                 int g, int c, int lane, bool frozen, RF &&refill) {
   using C = QC<Q, KR>;
   constexpr int T = C::T, LKR = C::LKR, LT = C::LT;
   static_assert(T > 1 && DO <= 3, "phased SUS check: q >= 16, degree <= 4");
@@ -1319,7 +1350,7 @@ __device__ __forceinline__ void sus_check_phased(const WaveArgs &a, const unsign
       release_stage(empty, lane);
       refill();
     }
-    const int az = rowtab[(size_t)(pke & 0xff) * Q + z] >> 7;  // h_e^-1 z
+    const int az = rowtab[(size_t)(pke & 0xff) * Q + z] >> 7;  // h_e^-1 z (rare: degree-1 check)
 #pragma unroll
     for (int k = 0; k < KR; ++k) acc[k] = (c * KR + k == az) ? (double)Q : 0.0;
     float *rs = rsm + (size_t)s * Q * 32 + lane + c * KR * 32;
@@ -1336,7 +1367,7 @@ __device__ __forceinline__ void sus_check_phased(const WaveArgs &a, const unsign
 #pragma unroll
     for (int t = 0; t < DO; ++t) {
       uint32_t ad[KR];
-      tab_addrs<Q, KR>(pay_u32 + (uint32_t)(t * Q * 128 + lane * 4), rowtab, sd->perm_o[t], c, ad);
+      row_addrs<Q, KR, RTS>(pay_u32 + (uint32_t)(t * Q * 128 + lane * 4), rt, rowtab, sd->perm_o[t], c, ad);
 #pragma unroll
       for (int k = 0; k < KR; ++k) v[t][k] = (double)lds_f32(ad[k]);
     }
@@ -1388,7 +1419,7 @@ __device__ __forceinline__ void sus_check_phased(const WaveArgs &a, const unsign
     }
     wht_bits<KR, 0, LKR>(acc);
     uint32_t ad[KR];
-    tab_addrs<Q, KR>(0u, rowtab, pke, c, ad);  // ad[k] = (h_e^-1 y) * 128: a = h_e^-1 y
+    row_addrs<Q, KR, RTS>(0u, rt, rowtab, pke, c, ad);  // ad[k] = (h_e^-1 y) * 128: a = h_e^-1 y
     unsigned char *rs = (unsigned char *)(rsm + (size_t)s * Q * 32 + lane);
 #pragma unroll
     for (int k = 0; k < KR; ++k) *(float *)(rs + ad[k]) = fmaxf((float)acc[k], 0.0f);
@@ -1449,6 +1480,10 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
     if (a.Tf)
       for (int k = threadIdx.x; k < 2 * Q * Q; k += blockDim.x) sp.tsm[k] = a.Tf[k];
   }
+  unsigned short *rtab = (unsigned short *)(sp.tsm + SS::TSM_F);
+  if constexpr (SS::RTS)
+    for (int k = threadIdx.x; k < Q * Q; k += blockDim.x) rtab[k] = a.c.rowtab[k];
+  const uint32_t rt = smem_u32(rtab);
   __syncthreads();
   const long long ntask = (long long)(*a.nactive) * ncols;
   constexpr bool PW = PWof<T>::v;
@@ -1521,7 +1556,7 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       double *stage_x = (double *)(sp.pay + (size_t)k * Sh::PAYA);
       if constexpr (SS::PHASED) {
         if (dv > 0) {
-#define SP(n) sus_check_phased<Q, KR, n>(a, hdr, pay_u32, stage_x, empty, last, xp, rsm, a.c.rowtab, g, c, lane, frozen, refill)
+#define SP(n) sus_check_phased<Q, KR, n, SS::RTS>(a, hdr, pay_u32, stage_x, empty, last, xp, rsm, rt, a.c.rowtab, g, c, lane, frozen, refill)
           switch (d - 1) {
             case 0: SP(0); break;
             case 1: SP(1); break;

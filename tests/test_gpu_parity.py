@@ -353,8 +353,8 @@ def _low_degree_code(p, N, M, seed):
     return rows, cols, vals, A, B
 
 
-@pytest.mark.parametrize("p", [5, 6])
-def test_low_degree_code_large_field_message_parity(gfq, p):
+@pytest.mark.parametrize("p,markov", [(5, False), (6, False), (6, True)])
+def test_low_degree_code_large_field_message_parity(gfq, p, markov):
     N, M = 30, 50
     for seed in range(300, 400):
         rows, cols, vals, A, B = _low_degree_code(p, N, M, seed)
@@ -369,11 +369,13 @@ def test_low_degree_code_large_field_message_parity(gfq, p):
     F = 45                                 # two blocks, ragged
     hard = rng.integers(0, 2, (F, M * p)).astype(np.uint8)
     pi = rng.uniform(0.02, 0.3, (F, M * p)).astype(np.float32)
+    T = synth.markov_uniform_jump(1 << p, 0.6) if markov else None
     for schedule in (0, 1):
-        prm = gfq.Params(schedule=schedule, max_iters=4, early_exit=False, keep_messages=True)
+        prm = gfq.Params(schedule=schedule, max_iters=4, early_exit=False, keep_messages=True, markov_T=T)
         x, it, ws = gfq.gfq_decode_evidence(gcode, torch.as_tensor(hard).cuda(), torch.as_tensor(pi).cuda(), prm)
         qg, rg, Qg = gfq.gfq_export_messages(gcode, F, ws, prm)
-        ref = oc.decode(hard, pi.astype(np.float64), schedule=schedule, max_iters=4, fixed=True, keep_messages=True)
+        ref = oc.decode(hard, pi.astype(np.float64), schedule=schedule, max_iters=4, fixed=True, keep_messages=True,
+                        T=T)
         assert float(np.max(np.abs(qg.cpu().numpy() - ref["q"]))) <= MSG_TOL
         assert float(np.max(np.abs(rg.cpu().numpy() - ref["r"]))) <= MSG_TOL
         assert float(np.max(np.abs(Qg.cpu().numpy() - ref["Q"]))) <= MSG_TOL
