@@ -192,6 +192,46 @@ int gfq_export_messages(const gfq_code *code, int n_frames, const void *workspac
 int gfq_decode_stats(const gfq_code *code, const void *workspace, size_t ws_bytes,
                      long long stats[4], void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Monte-Carlo front end (the steps before the decoder): source,
+ * encoding t = B^-1 A s (Eq. 1) and channel, on the device, so that BER
+ * sweeps (Table 1) run at GPU speed.
+ */
+typedef struct {
+    int channel;        /* GFQ_BSC (ch_param = f), GFQ_BEC (eps), GFQ_BIAWGN (sigma) */
+    double ch_param;
+    const double *markov_T; /* host q*q row-stochastic, or NULL = i.i.d. uniform source */
+    const double *src_pi0;  /* host q, law of s_0 for a Markov source; NULL = uniform */
+} gfq_sim_params;
+
+/* Device workspace for gfq_simulate of n_frames frames (0 on bad arguments). */
+size_t gfq_simulate_workspace_bytes(const gfq_code *code, int n_frames);
+
+/* Frames frame0 .. frame0+n_frames-1 of the stream `seed` (device outputs):
+ *   s_out   uint8 [n_frames][N]   source symbols (NULL to skip),
+ *   obs_out [n_frames][M*p]       channel output in the layout gfq_decode takes
+ *                                 (uint8 bits / {0,1,2=erased} / float32 y), or NULL,
+ *   t_out   uint8 [n_frames][M]   codeword symbols t = B^-1 A s (NULL: kept in
+ *                                 the workspace).
+ * Random numbers (so that a CPU program can draw the same ones): Philox4x32-10
+ * with key (seed mod 2^32, seed >> 32) and counter (j, frame mod 2^32,
+ * frame >> 32, purpose), purpose 1 = source, 2 = channel; u24(x) = (x >> 8) 2^-24.
+ *   i.i.d. source: symbol 4j+m = x_m mod q.
+ *   Markov source: u_k = u24(x_m) for k = 4j+m; s_0 = min{b : u_0 < C0[b]},
+ *     s_k = min{b : u_k < C[s_{k-1}][b]}, C0 / C the running sums (double, left
+ *     to right, last entry set to 1) of pi0 and of the rows of T.
+ *   BSC: transmitted bit 4j+m flips iff u24(x_m) < f;  BEC: erased (obs 2) iff
+ *     u24(x_m) < eps;  BI-AWGN: bits 2j, 2j+1 from one call, u1 = ((x_0 >> 8)
+ *     + 1) 2^-24, u2 = u24(x_1), rho = sqrt(-2 ln u1), noise rho cos(2 pi u2),
+ *     rho sin(2 pi u2); y = (1 - 2 bit) + sigma * noise in float32 (A16).
+ * Bits are LSB first (A2).  Errors: GFQ_EINVAL (bad arguments, workspace too
+ * small), GFQ_EUNSUPPORTED if B is not triangular up to a permutation (the
+ * encoder solves B t = A s by peeling rows with one unknown; the MN
+ * construction's B always is), GFQ_ECUDA.  Asynchronous on `stream`. */
+int gfq_simulate(const gfq_code *code, int n_frames, unsigned long long seed, long long frame0,
+                 const gfq_sim_params *params, unsigned char *s_out, void *obs_out,
+                 unsigned char *t_out, void *workspace, size_t ws_bytes, void *stream);
+
 /* Per-kernel timing for roofline reporting.  gfq_profile_enable(1) makes every
  * later decode call of the calling thread record a CUDA event pair around each
  * kernel it launches, on the decode's stream (accumulators are reset);

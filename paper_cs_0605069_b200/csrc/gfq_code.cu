@@ -201,6 +201,40 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   }
   const size_t U = lunit.size();
 
+  // Encoder support (gfq_simulate, Eq. 1): an order that solves B t = y row by
+  // row -- each row, when reached, has exactly one unsolved column of B
+  // ("peeling").  Exists for the MN construction (B triangular up to a
+  // permutation, reading A23); otherwise simulation is unsupported.
+  std::vector<int> peel;  // pairs (row r, noise column k solved by row r)
+  {
+    std::vector<int> unknown(M, 0);
+    std::vector<std::vector<int>> rows_of(M);
+    for (int i = 0; i < M; ++i)
+      for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e)
+        if (edge_var[e] >= N) { unknown[i]++; rows_of[edge_var[e] - N].push_back(i); }
+    std::vector<char> solved(M, 0), used(M, 0);
+    std::vector<int> stack;
+    for (int i = M - 1; i >= 0; --i)
+      if (unknown[i] == 1) stack.push_back(i);
+    while (!stack.empty()) {
+      const int i = stack.back();
+      stack.pop_back();
+      if (used[i] || unknown[i] != 1) continue;
+      used[i] = 1;
+      int k = -1;
+      for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e)
+        if (edge_var[e] >= N && !solved[edge_var[e] - N]) k = edge_var[e] - N;
+      solved[k] = 1;
+      peel.push_back(i);
+      peel.push_back(k);
+      for (int i2 : rows_of[k])
+        if (--unknown[i2] == 1 && !used[i2]) stack.push_back(i2);
+    }
+    if ((int)peel.size() != 2 * M) peel.clear();
+  }
+  std::vector<unsigned char> inv(q, 0);
+  for (int x = 1; x < q; ++x) inv[x] = (unsigned char)gf.inv(x);
+
   std::vector<unsigned char> mul((size_t)q * q);
   for (int x = 0; x < q; ++x)
     for (int y = 0; y < q; ++y) mul[x * q + y] = (unsigned char)gf.mul(x, y);
@@ -228,6 +262,8 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   const size_t o_sdesc = off; off += al(sizeof(SusDesc) * E);
   const size_t o_lvlcol = off; off += al(sizeof(LvlCol) * V);
   const size_t o_lunit = off; off += al(sizeof(LvlUnit) * U);
+  const size_t o_peel = off; off += al(sizeof(int) * peel.size());
+  const size_t o_inv = off; off += al(q);
   std::vector<unsigned char> host(off, 0);
   auto put = [&](size_t o, const void *src, size_t n) { if (n) memcpy(host.data() + o, src, n); };
   put(o_row, row_ptr.data(), sizeof(int) * (M + 1));
@@ -247,6 +283,8 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   put(o_sdesc, sdesc.data(), sizeof(SusDesc) * E);
   put(o_lvlcol, lcol.data(), sizeof(LvlCol) * V);
   put(o_lunit, lunit.data(), sizeof(LvlUnit) * U);
+  put(o_peel, peel.data(), sizeof(int) * peel.size());
+  put(o_inv, inv.data(), q);
 
   int dev = 0;
   cudaError_t ce = cudaGetDevice(&dev);
@@ -283,6 +321,8 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   c->d.sus_desc = (const SusDesc *)(b + o_sdesc);
   c->d.lvl_col = (const LvlCol *)(b + o_lvlcol);
   c->d.lvl_unit = (const LvlUnit *)(b + o_lunit);
+  c->d.peel = peel.empty() ? nullptr : (const int *)(b + o_peel);
+  c->d.inv = b + o_inv;
   *out = c;
   return GFQ_OK;
 }

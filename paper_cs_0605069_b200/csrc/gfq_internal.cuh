@@ -66,6 +66,8 @@ struct DevCode {
   const SusDesc *sus_desc;      // [E] canonical order
   const LvlCol *lvl_col;        // [V] level order (level_ptr delimits levels)
   const LvlUnit *lvl_unit;      // [U] U = sum over columns of max(dv, 1)
+  const int *peel;              // [2M] encoder order: (row, noise column solved), or null
+  const unsigned char *inv;     // [q]   GF(2^p) inverses (inv[0] = 0)
 };
 
 }  // namespace gfq
@@ -142,5 +144,24 @@ int launch_export(const WaveArgs &a, float *q_out, float *r_out, float *Q_out, c
 int launch_set_u64(unsigned long long *p, unsigned long long v, cudaStream_t s);
 int launch_trace(const WaveArgs &a, const unsigned char *truth, int *trace, int t, int tlen, cudaStream_t s);
 int launch_trace_fill(int *trace, int n_frames, int tlen, cudaStream_t s);
+
+// Monte-Carlo front end (gfq_sim.cu)
+struct SimArgs {
+  DevCode c;
+  int n_frames, nfb;
+  unsigned long long seed;
+  long long frame0;
+  int channel;
+  double param;
+  int markov;
+  const double *cum0;   // [q]   running sums of pi0 (device)
+  const double *cumT;   // [q*q] running sums of the rows of T (device)
+  unsigned char *s_blk; // [nfb][N][32]
+  unsigned char *t_blk; // [nfb][M][32]
+  unsigned char *s_out; // [F][N]
+  unsigned char *t_fm;  // [F][M]
+  void *obs;            // [F][M*p]
+};
+int launch_sim(const SimArgs &a, cudaStream_t s);
 
 }  // namespace gfq

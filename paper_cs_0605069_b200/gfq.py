@@ -24,7 +24,7 @@ GFQ_PUS, GFQ_SUS = 0, 1
 EXPORTS = ["gfq_last_error", "gfq_version", "gfq_code_create", "gfq_code_destroy", "gfq_code_info",
            "gfq_workspace_bytes", "gfq_decode", "gfq_decode_evidence", "gfq_workspace_bytes_host",
            "gfq_decode_host", "gfq_export_messages", "gfq_decode_stats", "gfq_profile_enable",
-           "gfq_profile_read", "gfq_kernel_name"]
+           "gfq_profile_read", "gfq_kernel_name", "gfq_simulate_workspace_bytes", "gfq_simulate"]
 GFQ_NKERNELS = 14
 
 
@@ -40,6 +40,11 @@ class gfq_params(ctypes.Structure):
                 ("early_exit", ctypes.c_int), ("markov_T", ctypes.c_void_p),
                 ("src_pi0", ctypes.c_void_p), ("keep_messages", ctypes.c_int),
                 ("trace_truth", ctypes.c_void_p), ("trace", ctypes.c_void_p)]
+
+
+class gfq_sim_params(ctypes.Structure):
+    _fields_ = [("channel", ctypes.c_int), ("ch_param", ctypes.c_double),
+                ("markov_T", ctypes.c_void_p), ("src_pi0", ctypes.c_void_p)]
 
 
 _lib = None
@@ -79,6 +84,10 @@ def lib() -> ctypes.CDLL:
         L.gfq_profile_enable.restype = i
         L.gfq_profile_read.argtypes = [vp, vp]
         L.gfq_profile_read.restype = i
+        L.gfq_simulate_workspace_bytes.argtypes = [vp, i]
+        L.gfq_simulate_workspace_bytes.restype = sz
+        L.gfq_simulate.argtypes = [vp, i, ctypes.c_ulonglong, ll, P(gfq_sim_params), vp, vp, vp, vp, sz, vp]
+        L.gfq_simulate.restype = i
         L.gfq_kernel_name.argtypes = [i]
         L.gfq_kernel_name.restype = ctypes.c_char_p
         _lib = L
@@ -249,3 +258,23 @@ def gfq_profile_read():
     n = (ctypes.c_longlong * GFQ_NKERNELS)()
     _check(lib().gfq_profile_read(ctypes.addressof(ms), ctypes.addressof(n)))
     return {lib().gfq_kernel_name(k).decode(): (ms[k], n[k]) for k in range(GFQ_NKERNELS)}
+
+
+def gfq_simulate(code: Code, n_frames: int, seed: int, channel: int, ch_param: float, frame0: int = 0,
+                 markov_T=None, src_pi0=None, want_t: bool = False, device="cuda", stream=None):
+    """Monte-Carlo frames on the device (include/gfq.h): returns (s [F][N] uint8,
+    obs [F][M*p] uint8 or float32, t [F][M] uint8 or None) as CUDA tensors."""
+    import torch
+    T = None if markov_T is None else np.ascontiguousarray(markov_T, dtype=np.float64)
+    p0 = None if src_pi0 is None else np.ascontiguousarray(src_pi0, dtype=np.float64)
+    prm = gfq_sim_params(int(channel), float(ch_param), None if T is None else T.ctypes.data,
+                         None if p0 is None else p0.ctypes.data)
+    F = int(n_frames)
+    s = torch.empty((F, code.N), dtype=torch.uint8, device=device)
+    obs = torch.empty((F, code.M * code.p), dtype=torch.float32 if channel == GFQ_BIAWGN else torch.uint8,
+                      device=device)
+    t = torch.empty((F, code.M), dtype=torch.uint8, device=device) if want_t else None
+    ws = alloc_workspace(lib().gfq_simulate_workspace_bytes(code.h, F), device)
+    _check(lib().gfq_simulate(code.h, F, int(seed) & 0xFFFFFFFFFFFFFFFF, int(frame0), ctypes.byref(prm),
+                              _dptr(s), _dptr(obs), _dptr(t), _dptr(ws), ws.numel(), _stream_ptr(stream)))
+    return s, obs, t
