@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-convergence", action="store_true")
     ap.add_argument("--conv-frames", type=int, default=1024)
     ap.add_argument("--schedules", default="pus,sus")
+    ap.add_argument("--host-gen", action="store_true",
+                    help="generate the frames with the host generator synth/ instead of gfq_simulate")
     return ap.parse_args()
 
 
@@ -220,14 +222,29 @@ def main():
     code = synth.code_for(cfg)
     gcode = gfq.Code.from_synth(code)
     # rank r decodes frames [r*F, (r+1)*F) of the config's stream
+    T = synth.markov_T_for(cfg)
     t_gen = time.perf_counter()
-    fr = synth.frames_for(cfg, code, shard.frame_range(rank, world, F), point=args.point)
+    if args.host_gen:
+        fr = synth.frames_for(cfg, code, shard.frame_range(rank, world, F), point=args.point)
+        obs_host = torch.from_numpy(fr.obs).pin_memory()
+        obs = obs_host.to("cuda", non_blocking=True)
+        truth = fr.s
+    else:
+        # Monte-Carlo front end on the device (gfq_simulate, counter-based Philox
+        # draws: the same frames for any rank count / subset)
+        param = cfg.ch_params[args.point]
+        if cfg.channel == synth.BIAWGN:
+            param = synth.awgn_sigma(param)
+        ch0 = {synth.BSC: gfq.GFQ_BSC, synth.BEC: gfq.GFQ_BEC, synth.BIAWGN: gfq.GFQ_BIAWGN}[cfg.channel]
+        s_dev, obs, _ = gfq.gfq_simulate(gcode, F, 0xBE7C0000 + cfg.cid * 64 + args.point, ch0, param,
+                                         frame0=shard.frame_range(rank, world, F)[0], markov_T=T)
+        obs_host = obs.cpu().pin_memory()
+        truth = s_dev.cpu().numpy()
+        fr = argparse.Namespace(channel=cfg.channel, ch_param=param, obs=None, s=truth)
+    torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
     ch = {synth.BSC: gfq.GFQ_BSC, synth.BEC: gfq.GFQ_BEC, synth.BIAWGN: gfq.GFQ_BIAWGN}[fr.channel]
-    T = synth.markov_T_for(cfg)
     params = {s: gfq.Params(ch, fr.ch_param, s, iters, early_exit=False, markov_T=T) for s in schedules}
-    obs_host = torch.from_numpy(fr.obs).pin_memory()
-    obs = obs_host.to("cuda", non_blocking=True)
     s_hat = torch.empty((F, cfg.N), dtype=torch.uint8, device="cuda")
     it = torch.empty(F, dtype=torch.int32, device="cuda")
     torch.cuda.synchronize()
@@ -330,7 +347,7 @@ def main():
             pc = gfq.Params(ch, fr.ch_param, s, cfg.max_iters, early_exit=True, markov_T=T)
             sh, ic, _ = gfq.gfq_decode(gcode, obs_c, pc, workspace=ws)
             its[s] = ic.cpu().numpy()
-            errs = (sh.cpu().numpy() != fr.s[:nf]).any(axis=1)
+            errs = (sh.cpu().numpy() != truth[:nf]).any(axis=1)
             its[("fer", s)] = float(errs.mean())
         conv = dict(frames=nf, max_iters=cfg.max_iters)
         for s in schedules:
@@ -351,7 +368,8 @@ def main():
         ncores = os.cpu_count() or 1
         si = 1 if cfg.q >= 64 else 2
         sf = max(1, min(ncores, 32))
-        dt, thr = oracle_sample_rate(cfg, code, fr, sf, si, [0 if s == gfq.GFQ_PUS else 1 for s in schedules])
+        sample = argparse.Namespace(channel=fr.channel, ch_param=fr.ch_param, obs=obs_host[:sf].numpy())
+        dt, thr = oracle_sample_rate(cfg, code, sample, sf, si, [0 if s == gfq.GFQ_PUS else 1 for s in schedules])
         t_full = dt * iters / si
         cpu = dict(value=len(schedules) * sf * cfg.N * cfg.p / t_full, unit="bit/s", cores=thr, kind="oracle",
                    sample="%d frames x %d iteration(s) per schedule, extrapolated linearly to %d iterations"
@@ -366,7 +384,9 @@ def main():
                         parallelism="frame-sharded dp%d (no collective)" % world,
                         l2="inputs larger than L2 (message state %.1f GB/GPU vs 126 MB)" %
                            (cfg.E * cfg.q * 4 * F * 2 / 1e9),
-                        workspace_gb=ws_bytes / 1e9, input_gen_s=t_gen),
+                        workspace_gb=ws_bytes / 1e9, input_gen_s=t_gen,
+                        input_gen="host synth/ (PCG64)" if args.host_gen else
+                        "device gfq_simulate (Philox4x32-10, seed 0x%x)" % (0xBE7C0000 + cfg.cid * 64 + args.point)),
             edge_msg_updates_per_s=edge_updates / (ms / 1e3),
             model_hbm_gbs=model_gbs,
             roofline=roof, cpu_baseline=cpu, e2e=e2e, clocks=clk,
