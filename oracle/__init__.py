@@ -60,7 +60,8 @@ def lib():
             L.o_unsatisfied.argtypes = [vp, vp, vp]
             L.o_unsatisfied.restype = i
             L.o_decode_frame.argtypes = [vp, i, i, i, vp, vp, vp, vp, vp, P(i), vp, vp, vp,
-                                         P(ctypes.c_long), vp, vp]
+                                         P(ctypes.c_long), vp, vp, i]
+            L.o_markov_prior_one.argtypes = [i, vp, vp, vp, vp, vp]
             L.o_decode_frame.restype = i
             _lib = L
     return _lib
@@ -130,6 +131,16 @@ def markov_prior(T, pi0, Q) -> np.ndarray:
     return P
 
 
+def markov_prior_one(T, pi0, left=None, right=None) -> np.ndarray:
+    T = np.ascontiguousarray(T, dtype=np.float64)
+    pi0 = np.ascontiguousarray(pi0, dtype=np.float64)
+    lf = None if left is None else np.ascontiguousarray(left, dtype=np.float64)
+    rt = None if right is None else np.ascontiguousarray(right, dtype=np.float64)
+    out = np.zeros(len(pi0), np.float64)
+    lib().o_markov_prior_one(len(pi0), _p(T), _p(pi0), _p(lf), _p(rt), _p(out))
+    return out
+
+
 # ---------------------------------------------------------------- code + decode
 class OCode:
     """H = [A B] from COO (rows = checks, cols = variables 0..N+M-1)."""
@@ -170,7 +181,8 @@ class OCode:
         return lib().o_unsatisfied(self._h, _p(x), _p(z))
 
     def decode(self, hard, pi, schedule: int = PUS, max_iters: int = 100, fixed: bool = False,
-               T=None, pi0=None, keep_messages: bool = False, threads: int = 0, s_true=None):
+               T=None, pi0=None, keep_messages: bool = False, threads: int = 0, s_true=None,
+               sus_gs: bool = False):
         """Decode frames. hard uint8 [F][M*p], pi float64 [F][M*p] (fp32 values may be
         passed: they are widened exactly).  Returns dict(xhat [F][V], iters [F],
         zero_norms [F], and q/r [F][E][q], Q [F][V][q] if keep_messages; with the true
@@ -200,7 +212,8 @@ class OCode:
                              _p(qm[f]) if keep_messages else None,
                              _p(rm[f]) if keep_messages else None,
                              _p(Qm[f]) if keep_messages else None, ctypes.byref(z),
-                             None if st is None else _p(st[f]), None if tr is None else _p(tr[f]))
+                             None if st is None else _p(st[f]), None if tr is None else _p(tr[f]),
+                             int(bool(sus_gs)))
             iters[f] = it.value
             zn[f] = z.value
 

@@ -219,6 +219,33 @@ void o_markov_prior(int q, int N, const double *T, const double *pi0,
     }
 }
 
+/* One symbol of Eq. (6) with the neighbours supplied separately (the prior
+ * refreshed inside the SUS sweep, reading A34): left = Q of symbol i-1 or
+ * NULL (left factor pi0(b), A10), right = Q of symbol i+1 or NULL (right
+ * factor 1).  Normalised over b. */
+void o_markov_prior_one(int q, const double *T, const double *pi0,
+                        const double *left, const double *right, double *P)
+{
+    double s = 0.0;
+    for (int b = 0; b < q; ++b) {
+        double v = 0.0;
+        if (!left && !right) {
+            v = pi0[b];
+        } else if (!left) {
+            for (int c = 0; c < q; ++c) v += pi0[b] * T[b * q + c] * right[c];
+        } else if (!right) {
+            for (int a = 0; a < q; ++a) v += left[a] * T[a * q + b];
+        } else {
+            for (int a = 0; a < q; ++a)
+                for (int c = 0; c < q; ++c) v += left[a] * T[a * q + b] * T[b * q + c] * right[c];
+        }
+        P[b] = v;
+        s += v;
+    }
+    if (s > 0.0)
+        for (int b = 0; b < q; ++b) P[b] /= s;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Code object: H = [A B]; rows = checks, columns = x = [s; n]   */
 /* Canonical edge order: column-major (j ascending, then i ascending).      */
@@ -371,12 +398,18 @@ static int correct_source_bits(int p, int N, const uint8_t *x, const uint8_t *s)
  *          equal to the true source s (t = 0: the clipped priors; t >= 1: after
  *          iteration t).  After an early exit at t0 the estimate is frozen, so
  *          trace[t] = trace[t0] for t > t0.
+ *   sus_gs: SUS with a Markov source only -- the source prior refreshed inside
+ *          the sweep (reading A34, "during the vertical pass"):
+ *          just before column j < N is updated, p_j = Eq. (6) from the
+ *          posterior of j-1 computed earlier in THIS sweep and the posterior of
+ *          j+1 from the previous sweep (none at t = 1: right factor 1); no
+ *          post-iteration refresh.  0: the post-iteration snapshot (A9).
  */
 int o_decode_frame(const ocode *c, int schedule, int max_iters, int fixed,
                    const uint8_t *hard, const double *pi, const double *T,
                    const double *pi0_in, uint8_t *xhat, int *iters,
                    double *qmsg_out, double *rmsg_out, double *Q_out,
-                   long *zero_norms, const uint8_t *s_true, int *trace)
+                   long *zero_norms, const uint8_t *s_true, int *trace, int sus_gs)
 {
     const int p = c->p, q = c->q, N = c->N, M = c->M, V = c->V;
     const long E = c->E;
@@ -385,6 +418,8 @@ int o_decode_frame(const ocode *c, int schedule, int max_iters, int fixed,
     double *rmsg = (double *)calloc((size_t)E * q, sizeof(double));
     double *Q = (double *)malloc(sizeof(double) * (size_t)V * q);
     double *pi0 = (double *)malloc(sizeof(double) * (size_t)q);
+    const int gs = (sus_gs && schedule == 1 && T != NULL);
+    double *Qprev = gs ? (double *)malloc(sizeof(double) * (size_t)V * q) : NULL;
     uint8_t *z = (uint8_t *)malloc((size_t)M);
     uint8_t *rsym = (uint8_t *)malloc((size_t)M);
     uint8_t *x = (uint8_t *)malloc((size_t)V);
@@ -446,11 +481,21 @@ int o_decode_frame(const ocode *c, int schedule, int max_iters, int fixed,
             /* SUS: for each column j in index order (A7):
              * step 1: partial horizontal pass, r_ij for all i in column j, from the current q's;
              * step 2: partial vertical pass over column j. */
+            if (gs && t > 1) memcpy(Qprev, Q, sizeof(double) * (size_t)V * q);
             for (int j = 0; j < V; ++j) {
                 for (int e = c->col_ptr[j]; e < c->col_ptr[j + 1]; ++e)
                     check_edge(c, e, z, qmsg, scratch_q, scratch_h, rmsg + (size_t)e * q);
+                if (gs && j < N) /* within-sweep prior (A34) */
+                    o_markov_prior_one(q, T, pi0, j > 0 ? Q + (size_t)(j - 1) * q : NULL,
+                                       (t > 1 && j < N - 1) ? Qprev + (size_t)(j + 1) * q : NULL,
+                                       prior + (size_t)j * q);
                 for (int e = c->col_ptr[j]; e < c->col_ptr[j + 1]; ++e)
                     zn += var_edge(c, e, prior + (size_t)j * q, rmsg, qmsg + (size_t)e * q);
+                if (gs && j < N) { /* Q_j now: the next column's left neighbour */
+                    int e0 = c->col_ptr[j], zf;
+                    o_posterior(q, c->col_ptr[j + 1] - e0, prior + (size_t)j * q, rmsg + (size_t)e0 * q,
+                                Q + (size_t)j * q, &zf);
+                }
             }
         }
         /* Pseudo-posterior Eq. (5) and clipping (SUS step 4, A8). */
@@ -470,7 +515,7 @@ int o_decode_frame(const ocode *c, int schedule, int max_iters, int fixed,
         if (pass && !fixed) break;
         if (*iters < 0) memcpy(xhat, x, (size_t)V);
         /* Re-estimate the source priors after the iteration (Eq. 6; A9). */
-        if (T && t < max_iters) {
+        if (T && !gs && t < max_iters) {
             double *P = (double *)malloc(sizeof(double) * (size_t)N * q);
             o_markov_prior(q, N, T, pi0, Q, P);
             memcpy(prior, P, sizeof(double) * (size_t)N * q);
@@ -485,6 +530,6 @@ int o_decode_frame(const ocode *c, int schedule, int max_iters, int fixed,
     if (Q_out) memcpy(Q_out, Q, sizeof(double) * (size_t)V * q);
     if (zero_norms) *zero_norms = zn;
     free(prior); free(qmsg); free(rmsg); free(Q); free(pi0); free(z); free(rsym);
-    free(x); free(scratch_q); free(scratch_h);
+    free(x); free(scratch_q); free(scratch_h); free(Qprev);
     return 0;
 }

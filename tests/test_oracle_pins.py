@@ -623,3 +623,67 @@ def test_embedded_binary_chain_matches_bit_chain():
     # symmetric 2S: uniform bits, so the symbol law is 1/2 * prod of the in-symbol transitions
     pi = [0.5 * T2[b & 1, (b >> 1) & 1] * T2[(b >> 1) & 1, (b >> 2) & 1] for b in range(8)]
     assert np.allclose(synth.stationary(T8), pi, atol=1e-12)
+
+
+# ----------------------------------------------------------------------------- within-sweep prior (A34, f2)
+def test_markov_prior_one_matches_eq6_block():
+    """The per-symbol prior with explicit neighbours equals the (pinned) Eq. (6)
+    block prior at an interior symbol and at both boundaries."""
+    rng = np.random.default_rng(4)
+    q, N = 4, 5
+    T = rng.random((q, q)); T /= T.sum(axis=1, keepdims=True)
+    pi0 = synth.stationary(T)
+    Q = rng.random((N, q)); Q /= Q.sum(axis=1, keepdims=True)
+    P = oracle.markov_prior(T, pi0, Q)
+    assert np.allclose(oracle.markov_prior_one(T, pi0, Q[1], Q[3]), P[2], atol=1e-14)
+    assert np.allclose(oracle.markov_prior_one(T, pi0, None, Q[1]), P[0], atol=1e-14)
+    assert np.allclose(oracle.markov_prior_one(T, pi0, Q[N - 2], None), P[N - 1], atol=1e-14)
+    assert np.allclose(oracle.markov_prior_one(T, pi0, None, None), pi0, atol=1e-14)
+
+
+def _two_source_chain(s0=1):
+    """GF(2): sources s0, s1 (s1 in no check), one check s0 + n0 = z0 with a
+    noise bit known to be 0: s0 is decoded exactly in the first sweep."""
+    oc = oracle.OCode(1, POLY[1], 2, 1, np.array([0, 0], np.int32), np.array([0, 2], np.int32),
+                      np.array([1, 1], np.uint8))
+    hard = np.array([[s0]], np.uint8)                 # r = t = s0 (B = [1], A = [1 0])
+    pi = np.array([[1e-12]])
+    return oc, hard, pi
+
+
+def test_within_sweep_prior_closed_form():
+    """SUS with the prior refreshed inside the sweep: after ONE iteration the
+    unchecked source s1 already carries T[s0] (its left neighbour was decoded
+    earlier in the same sweep); with the post-iteration snapshot (A9) it is
+    still pi0 after one iteration and T[s0] after two."""
+    T = np.array([[0.9, 0.1], [0.2, 0.8]])
+    pi0 = synth.stationary(T)
+    oc, hard, pi = _two_source_chain(1)
+    gs1 = oc.decode(hard, pi, schedule=oracle.SUS, max_iters=1, fixed=True, T=T, pi0=pi0, keep_messages=True,
+                    sus_gs=True)
+    assert np.allclose(gs1["Q"][0, 0], [0.0, 1.0], atol=1e-9)
+    assert np.allclose(gs1["Q"][0, 1], T[1], atol=1e-9)
+    sn1 = oc.decode(hard, pi, schedule=oracle.SUS, max_iters=1, fixed=True, T=T, pi0=pi0, keep_messages=True)
+    assert np.allclose(sn1["Q"][0, 1], pi0, atol=1e-12)
+    sn2 = oc.decode(hard, pi, schedule=oracle.SUS, max_iters=2, fixed=True, T=T, pi0=pi0, keep_messages=True)
+    assert np.allclose(sn2["Q"][0, 1], T[1], atol=1e-9)
+    # second GS sweep: s0's prior now has the right factor from s1's first-sweep posterior
+    gs2 = oc.decode(hard, pi, schedule=oracle.SUS, max_iters=2, fixed=True, T=T, pi0=pi0, keep_messages=True,
+                    sus_gs=True)
+    assert np.allclose(gs2["Q"][0, 1], T[1], atol=1e-9)
+
+
+def test_within_sweep_prior_reduces_to_iid_for_memoryless_T():
+    """T with identical rows (no memory): Eq. (6) gives the row itself at every
+    symbol, so the within-sweep SUS decode equals the i.i.d. decode."""
+    c = synth.CONFIGS["C2"]
+    code = synth.code_for(c)
+    fr = synth.frames_for(c, code, range(3))
+    oc = oracle.OCode.from_synth(code)
+    hard, pi = oracle.frontend(fr.channel, fr.ch_param, fr.obs)
+    row = np.array([0.4, 0.3, 0.2, 0.1])
+    T = np.tile(row, (4, 1))
+    a = oc.decode(hard, pi, schedule=oracle.SUS, max_iters=4, fixed=True, T=T, pi0=row, keep_messages=True,
+                  sus_gs=True)
+    b = oc.decode(hard, pi, schedule=oracle.SUS, max_iters=4, fixed=True, pi0=row, keep_messages=True)
+    assert np.max(np.abs(a["Q"] - b["Q"])) < 1e-12 and np.array_equal(a["iters"], b["iters"])
