@@ -46,6 +46,7 @@ extern "C" {
 
 typedef enum { GFQ_BSC = 0, GFQ_BEC = 1, GFQ_BIAWGN = 2 } gfq_channel;
 typedef enum { GFQ_PUS = 0, GFQ_SUS = 1 } gfq_schedule;
+typedef enum { GFQ_PRIOR_SNAPSHOT = 0, GFQ_PRIOR_IN_SWEEP = 1 } gfq_prior_update;
 
 /* Opaque, immutable after creation; may be shared by concurrent decodes on
  * different streams (each with its own workspace). */
@@ -89,6 +90,18 @@ typedef struct {
      * kernel reading N bytes of estimates per frame). */
     const unsigned char *trace_truth;
     int *trace;
+    /* When the Markov source prior is refreshed (markov_T != NULL only):
+     *   GFQ_PRIOR_SNAPSHOT (0): after every iteration, p^(t) = Eq. (7) of the
+     *     posterior snapshot Q^(t), used by the vertical pass of iteration t+1
+     *     (reading A9) -- both schedules;
+     *   GFQ_PRIOR_IN_SWEEP (1): SUS only -- "during the vertical pass"
+     *     (reading A34): just before source column j is updated, p_j
+     *     = Eq. (7) from the posterior of j-1 computed earlier in THIS sweep
+     *     and that of j+1 from the previous sweep (none in sweep 1: factor 1);
+     *     boundaries as A10.  The source columns then form a chain, so the
+     *     sweep runs about N dependency levels instead of ~13.
+     * GFQ_EINVAL for other values or GFQ_PRIOR_IN_SWEEP with PUS. */
+    int prior_update;
 } gfq_params;
 
 /* Thread-local description of the last error (never NULL). */

@@ -399,26 +399,43 @@ struct Extra {
   static constexpr int rows = MARKOV ? (2 * Q > P ? 2 * Q : P) : P;
 };
 
+// Which Markov neighbour posteriors source column j reads (bit 0: j-1, bit 1:
+// j+1), and from where: snapshot mode (A9) both from Q^(t-1) (qs_old) from
+// iteration 2 on; in-sweep mode (A34) j-1 from this sweep (qs_new, written by
+// an earlier level) and j+1 from the previous sweep (qs_old, none in sweep 1).
+__device__ __forceinline__ int markov_nbrs(const WaveArgs &a, int j) {
+  const int N = a.c.N;
+  if (a.qs_old == nullptr) return 0;
+  if (a.gs) return (j > 0 ? 1 : 0) | ((a.t > 1 && j < N - 1) ? 2 : 0);
+  if (a.t <= 1) return 0;
+  return (j > 0 ? 1 : 0) | (j < N - 1 ? 2 : 0);
+}
+
 template <int Q, bool MARKOV>
 __device__ __forceinline__ uint32_t extras_bytes(const WaveArgs &a, int j) {
   constexpr int P = ilog2(Q);
   const int N = a.c.N;
   if (j >= N) return P * 128;
-  if (MARKOV && a.t > 1 && a.qs_old) return (uint32_t)((j > 0) + (j < N - 1)) * Q * 128;
+  if (MARKOV) {
+    const int nb = markov_nbrs(a, j);
+    return (uint32_t)((nb & 1) + (nb >> 1)) * Q * 128;
+  }
   return 0;
 }
 
 // noise symbol -> its p per-bit flip probabilities (slot 0); Markov source
-// symbol at iteration >= 2 -> posterior snapshots of j-1 (slot 0) and j+1 (slot 1)
+// symbol -> posteriors of j-1 (slot 0) and j+1 (slot 1) as markov_nbrs says
 template <int Q, bool MARKOV>
 __device__ __forceinline__ void issue_extras(const WaveArgs &a, int fb, int j, unsigned char *dst, uint64_t *bar) {
   constexpr int P = ilog2(Q);
   const int N = a.c.N;
   if (j >= N) {
     bulk_g2s(dst, a.pi + ((size_t)fb * a.c.M * P + (size_t)(j - N) * P) * 32, P * 128, bar);
-  } else if (MARKOV && a.t > 1 && a.qs_old) {
-    if (j > 0) bulk_g2s(dst, a.qs_old + ((size_t)fb * N + (j - 1)) * Q * 32, Q * 128, bar);
-    if (j < N - 1) bulk_g2s(dst + Q * 128, a.qs_old + ((size_t)fb * N + (j + 1)) * Q * 32, Q * 128, bar);
+  } else if (MARKOV) {
+    const int nb = markov_nbrs(a, j);
+    const float *left = a.gs ? a.qs_new : a.qs_old;
+    if (nb & 1) bulk_g2s(dst, left + ((size_t)fb * N + (j - 1)) * Q * 32, Q * 128, bar);
+    if (nb & 2) bulk_g2s(dst + Q * 128, a.qs_old + ((size_t)fb * N + (j + 1)) * Q * 32, Q * 128, bar);
   }
 }
 
@@ -429,6 +446,9 @@ __device__ __forceinline__ void issue_extras(const WaveArgs &a, int fb, int j, u
 //  - source symbol, Markov, iteration t >= 2: Eq. (7) from the
 //    posterior snapshot Q^(t-1) of the neighbours (reading A9), boundaries A10:
 //      p(b) = [sum_a Q_{j-1}(a) T_ab] * [sum_c T_bc Q_{j+1}(c)]
+//  - SUS with the in-sweep prior (reading A34): the same formula
+//    with Q_{j-1} of this sweep and Q_{j+1} of the previous one (markov_nbrs);
+//    a missing neighbour gives the factor pi0(b) (left) or 1 (right)
 template <int Q, int KR, bool MARKOV>
 __device__ __forceinline__ void prior_from(const WaveArgs &a, int j, int c, int lane, const float *ex,
                                            const float *Tsm, double (&pr)[KR]) {
@@ -454,7 +474,8 @@ __device__ __forceinline__ void prior_from(const WaveArgs &a, int j, int c, int 
     }
     return;
   }
-  if (!MARKOV || a.t <= 1 || a.qs_old == nullptr) {
+  const int nb = MARKOV ? markov_nbrs(a, j) : 0;
+  if (nb == 0) {
 #pragma unroll
     for (int k = 0; k < KR; ++k) pr[k] = __ldg(a.pi0 + c * KR + k);
     return;
@@ -469,7 +490,7 @@ __device__ __forceinline__ void prior_from(const WaveArgs &a, int j, int c, int 
   const float *exr = ex + Q * 32;  // rows of j+1 (slot 1)
 #pragma unroll
   for (int k = 0; k < KR; ++k) { L[k] = 0.0f; R[k] = 0.0f; }
-  if (j > 0) {
+  if (nb & 1) {
 #pragma unroll 4
     for (int x = 0; x < Q; ++x) {
       const float qv = exl[x * 32 + lane];
@@ -478,7 +499,7 @@ __device__ __forceinline__ void prior_from(const WaveArgs &a, int j, int c, int 
       for (int k = 0; k < KR; ++k) L[k] = fmaf(qv, trow[k], L[k]);
     }
   }
-  if (j < N - 1) {
+  if (nb & 2) {
 #pragma unroll 4
     for (int x = 0; x < Q; ++x) {
       const float qv = exr[x * 32 + lane];
@@ -489,8 +510,8 @@ __device__ __forceinline__ void prior_from(const WaveArgs &a, int j, int c, int 
   }
 #pragma unroll
   for (int k = 0; k < KR; ++k) {
-    const double l = (j > 0) ? (double)L[k] : __ldg(a.pi0 + c * KR + k);
-    const double r = (j < N - 1) ? (double)R[k] : 1.0;
+    const double l = (nb & 1) ? (double)L[k] : __ldg(a.pi0 + c * KR + k);
+    const double r = (nb & 2) ? (double)R[k] : 1.0;
     pr[k] = l * r;
   }
 }
@@ -1475,6 +1496,9 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
   extern __shared__ __align__(128) unsigned char smem[];
   const SmemPtrs sp = smem_ptrs<Sh, S, G>(smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // Programmatic dependent launch (levels are launched back to back, sus_launch):
+  // let the next level's CTAs start their prologue now; they wait below.
+  asm volatile("griddepcontrol.launch_dependents;");
   if (threadIdx.x == 0) init_bars<S, G>(sp.bars, T);
   if constexpr (MARKOV) {
     if (a.Tf)
@@ -1485,6 +1509,9 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
     for (int k = threadIdx.x; k < Q * Q; k += blockDim.x) rtab[k] = a.c.rowtab[k];
   const uint32_t rt = smem_u32(rtab);
   __syncthreads();
+  // everything below reads what the previous level (or iteration) wrote:
+  // wait until that grid has completed and its memory is visible
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const long long ntask = (long long)(*a.nactive) * ncols;
   constexpr bool PW = PWof<T>::v;
   if (PW && warp == 0) {
@@ -1708,7 +1735,21 @@ static int sus_launch(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
   if (SS::SMEM > 232448) return too_big("k_sus");
   auto k = k_sus<Q, KR, DM, DV, MK, NS, G>;
   const int grid = grid_for(k, SS::THREADS, SS::SMEM, ((long long)a.nfb * ncols + G - 1) / G);
-  k<<<grid, SS::THREADS, SS::SMEM, s>>>(a, lb, ncols);
+  // programmatic dependent launch: the kernel waits (griddepcontrol.wait) for
+  // the preceding grid before touching its outputs, so its launch and prologue
+  // overlap the previous level's tail (the in-sweep prior runs ~N levels)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(SS::THREADS);
+  cfg.dynamicSmemBytes = SS::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k, a, lb, ncols);
+  if (e != cudaSuccess) return cuda_fail(e, "k_sus");
   return check_launch("k_sus");
 }
 

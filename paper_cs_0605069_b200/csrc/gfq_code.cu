@@ -147,23 +147,32 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   // sharing a check with j; columns of one level share no check, so running a
   // level's columns concurrently, levels in order, reads exactly the values
   // the serial sweep reads.
-  std::vector<int> lvl(V, 0), rowlvl(M, 0);
-  int nlev = 0;
-  for (int j = 0; j < V; ++j) {
-    int L = 0;
-    for (int k = col_ptr[j]; k < col_ptr[j + 1]; ++k) L = std::max(L, rowlvl[edge_check[col_edge[k]]]);
-    L += 1;
-    lvl[j] = L;
-    for (int k = col_ptr[j]; k < col_ptr[j + 1]; ++k) rowlvl[edge_check[col_edge[k]]] = L;
-    nlev = std::max(nlev, L);
-  }
-  std::vector<int> level_ptr(nlev + 1, 0), level_cols(V);
-  for (int j = 0; j < V; ++j) level_ptr[lvl[j]]++;      // lvl in 1..nlev -> slot lvl
-  for (int L = 0; L < nlev; ++L) level_ptr[L + 1] += level_ptr[L];
-  {
+  // With the Markov prior refreshed inside the sweep (GFQ_PRIOR_IN_SWEEP,
+  // reading A34) source column j also reads the posterior of column j-1 of
+  // the same sweep: chain = true adds that dependency (level(j) > level(j-1)
+  // for 0 < j < N).
+  auto levels = [&](bool chain, std::vector<int> &level_ptr, std::vector<int> &level_cols) {
+    std::vector<int> lvl(V, 0), rowlvl(M, 0);
+    int nlev = 0;
+    for (int j = 0; j < V; ++j) {
+      int L = (chain && j > 0 && j < N) ? lvl[j - 1] : 0;
+      for (int k = col_ptr[j]; k < col_ptr[j + 1]; ++k) L = std::max(L, rowlvl[edge_check[col_edge[k]]]);
+      L += 1;
+      lvl[j] = L;
+      for (int k = col_ptr[j]; k < col_ptr[j + 1]; ++k) rowlvl[edge_check[col_edge[k]]] = L;
+      nlev = std::max(nlev, L);
+    }
+    level_ptr.assign(nlev + 1, 0);
+    level_cols.assign(V, 0);
+    for (int j = 0; j < V; ++j) level_ptr[lvl[j]]++;      // lvl in 1..nlev -> slot lvl
+    for (int L = 0; L < nlev; ++L) level_ptr[L + 1] += level_ptr[L];
     std::vector<int> fill(level_ptr.begin(), level_ptr.end() - 1);
     for (int j = 0; j < V; ++j) level_cols[fill[lvl[j] - 1]++] = j;
-  }
+    return nlev;
+  };
+  std::vector<int> level_ptr, level_cols, level_ptr_gs, level_cols_gs;
+  const int nlev = levels(false, level_ptr, level_cols);
+  const int nlev_gs = levels(true, level_ptr_gs, level_cols_gs);
 
   // static task tables (see gfq_internal.cuh)
   std::vector<CheckDesc> cdesc(M);
@@ -186,19 +195,25 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
       if (k != e) sdesc[cpos].perm_o[t++] = edge_perm[k];
     sdesc[cpos].perm_e = edge_perm[e];
   }
-  std::vector<LvlCol> lcol(V);
-  std::vector<LvlUnit> lunit;
-  lunit.reserve(E + V);
-  for (int k = 0; k < V; ++k) {
-    const int j = level_cols[k];
-    const int e0 = col_ptr[j], dv = col_ptr[j + 1] - e0;
-    lcol[k] = LvlCol{j, e0, dv, (int)lunit.size()};
-    if (dv == 0) lunit.push_back(LvlUnit{0, 0, 0, 0});
-    for (int s = 0; s < dv; ++s) {
-      const int e = col_edge[e0 + s], i = edge_check[e];
-      lunit.push_back(LvlUnit{row_ptr[i], row_ptr[i + 1] - row_ptr[i], e - row_ptr[i], i});
+  auto level_tables = [&](const std::vector<int> &cols, std::vector<LvlCol> &lcol, std::vector<LvlUnit> &lunit) {
+    lcol.resize(V);
+    lunit.clear();
+    lunit.reserve(E + V);
+    for (int k = 0; k < V; ++k) {
+      const int j = cols[k];
+      const int e0 = col_ptr[j], dv = col_ptr[j + 1] - e0;
+      lcol[k] = LvlCol{j, e0, dv, (int)lunit.size()};
+      if (dv == 0) lunit.push_back(LvlUnit{0, 0, 0, 0});
+      for (int s = 0; s < dv; ++s) {
+        const int e = col_edge[e0 + s], i = edge_check[e];
+        lunit.push_back(LvlUnit{row_ptr[i], row_ptr[i + 1] - row_ptr[i], e - row_ptr[i], i});
+      }
     }
-  }
+  };
+  std::vector<LvlCol> lcol, lcol_gs;
+  std::vector<LvlUnit> lunit, lunit_gs;
+  level_tables(level_cols, lcol, lunit);
+  level_tables(level_cols_gs, lcol_gs, lunit_gs);
   const size_t U = lunit.size();
 
   // Encoder support (gfq_simulate, Eq. 1): an order that solves B t = y row by
@@ -262,6 +277,8 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   const size_t o_sdesc = off; off += al(sizeof(SusDesc) * E);
   const size_t o_lvlcol = off; off += al(sizeof(LvlCol) * V);
   const size_t o_lunit = off; off += al(sizeof(LvlUnit) * U);
+  const size_t o_lvlcol_gs = off; off += al(sizeof(LvlCol) * V);
+  const size_t o_lunit_gs = off; off += al(sizeof(LvlUnit) * U);
   const size_t o_peel = off; off += al(sizeof(int) * peel.size());
   const size_t o_inv = off; off += al(q);
   std::vector<unsigned char> host(off, 0);
@@ -283,6 +300,8 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   put(o_sdesc, sdesc.data(), sizeof(SusDesc) * E);
   put(o_lvlcol, lcol.data(), sizeof(LvlCol) * V);
   put(o_lunit, lunit.data(), sizeof(LvlUnit) * U);
+  put(o_lvlcol_gs, lcol_gs.data(), sizeof(LvlCol) * V);
+  put(o_lunit_gs, lunit_gs.data(), sizeof(LvlUnit) * U);
   put(o_peel, peel.data(), sizeof(int) * peel.size());
   put(o_inv, inv.data(), q);
 
@@ -300,6 +319,8 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   c->p = p; c->q = q; c->N = N; c->M = M; c->V = V; c->poly = poly; c->E = E;
   c->max_cdeg = max_cdeg; c->max_vdeg = max_vdeg; c->n_levels = nlev; c->device = dev;
   c->level_ptr_h = level_ptr;
+  c->n_levels_gs = nlev_gs;
+  c->level_ptr_gs_h = level_ptr_gs;
   c->dev_blob = blob;
   unsigned char *b = (unsigned char *)blob;
   c->d.p = p; c->d.q = q; c->d.N = N; c->d.M = M; c->d.V = V; c->d.E = E;
@@ -321,6 +342,8 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   c->d.sus_desc = (const SusDesc *)(b + o_sdesc);
   c->d.lvl_col = (const LvlCol *)(b + o_lvlcol);
   c->d.lvl_unit = (const LvlUnit *)(b + o_lunit);
+  c->lvl_col_gs = (const LvlCol *)(b + o_lvlcol_gs);
+  c->lvl_unit_gs = (const LvlUnit *)(b + o_lunit_gs);
   c->d.peel = peel.empty() ? nullptr : (const int *)(b + o_peel);
   c->d.inv = b + o_inv;
   *out = c;

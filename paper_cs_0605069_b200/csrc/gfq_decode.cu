@@ -86,6 +86,14 @@ static int check_params(const gfq_code *c, const gfq_params *prm, bool need_chan
       if (std::fabs(s - 1.0) > 1e-6) { set_error("markov_T row is not stochastic"); return GFQ_EINVAL; }
     }
   }
+  if (prm->prior_update != GFQ_PRIOR_SNAPSHOT && prm->prior_update != GFQ_PRIOR_IN_SWEEP) {
+    set_error("bad prior_update");
+    return GFQ_EINVAL;
+  }
+  if (prm->prior_update == GFQ_PRIOR_IN_SWEEP && prm->schedule != GFQ_SUS) {
+    set_error("prior_update = GFQ_PRIOR_IN_SWEEP needs schedule = GFQ_SUS (reading A34)");
+    return GFQ_EINVAL;
+  }
   if ((prm->trace == nullptr) != (prm->trace_truth == nullptr)) {
     set_error("trace and trace_truth must both be set or both be NULL");
     return GFQ_EINVAL;
@@ -271,6 +279,13 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
     a.Tf = prm->markov_T ? at<float>(ws, L.Tf) : nullptr;
     a.pi0 = at<double>(ws, L.pi0);
     a.markov = prm->markov_T != nullptr;
+    a.gs = a.markov && prm->schedule == GFQ_SUS && prm->prior_update == GFQ_PRIOR_IN_SWEEP;
+    if (a.gs) {  // the level schedule with the source chain (gfq_code.cu)
+      a.c.lvl_col = c->lvl_col_gs;
+      a.c.lvl_unit = c->lvl_unit_gs;
+    }
+    const std::vector<int> &lptr = a.gs ? c->level_ptr_gs_h : c->level_ptr_h;
+    const int nlev = a.gs ? c->n_levels_gs : c->n_levels;
     a.early_exit = prm->early_exit ? 1 : 0;
     a.t = 1;
     float *qs[2] = {at<float>(ws, L.qs0), at<float>(ws, L.qs1)};
@@ -286,6 +301,7 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
       // x^(0): the clipped priors; no posterior snapshot is written
       WaveArgs a0 = a;
       a0.qs_new = nullptr;
+      a0.gs = 0;
       RUN(K_CLIP, launch_clip_priors(a0, st));
       if (tracing) RUN(K_TRACE, launch_trace(a, prm->trace_truth, prm->trace, 0, tlen, st));
     }
@@ -305,8 +321,8 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
         RUN(K_CN, launch_cn(a, st));
         RUN(K_VN, launch_vn(a, st));
       } else {
-        for (int lv = 0; lv < c->n_levels; ++lv) {
-          const int lb = c->level_ptr_h[lv], n = c->level_ptr_h[lv + 1] - lb;
+        for (int lv = 0; lv < nlev; ++lv) {
+          const int lb = lptr[lv], n = lptr[lv + 1] - lb;
           if (n > 0) RUN(K_SUS, launch_sus_level(a, lb, n, st));
         }
       }

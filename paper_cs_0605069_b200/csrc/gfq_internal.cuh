@@ -79,6 +79,10 @@ struct gfq_code {
   int max_cdeg, max_vdeg, n_levels;
   int device;
   std::vector<int> level_ptr_h;
+  int n_levels_gs;                  // the level schedule with the in-sweep prior chain (A34)
+  std::vector<int> level_ptr_gs_h;
+  const gfq::LvlCol *lvl_col_gs;    // device, same layout as DevCode::lvl_col
+  const gfq::LvlUnit *lvl_unit_gs;
   void *dev_blob;  // one cudaMalloc holding every device table
   gfq::DevCode d;
 };
@@ -122,6 +126,7 @@ struct WaveArgs {
   const float *Tf;      // [2*q*q] fp32 copies of T (row-major) and of T^T, or null
   const double *pi0;    // [q]
   int markov;
+  int gs;               // SUS with the Markov prior refreshed inside the sweep (A34)
   int t;                // current iteration (1-based)
   int early_exit;
 };

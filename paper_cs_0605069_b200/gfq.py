@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("GFQ_LIB_PATH") or os.path.join(_HERE, "libgfq.so")
 GFQ_OK, GFQ_EINVAL, GFQ_ENOMEM, GFQ_ECUDA, GFQ_EUNSUPPORTED = 0, -1, -2, -3, -4
 GFQ_BSC, GFQ_BEC, GFQ_BIAWGN = 0, 1, 2
 GFQ_PUS, GFQ_SUS = 0, 1
+GFQ_PRIOR_SNAPSHOT, GFQ_PRIOR_IN_SWEEP = 0, 1
 
 # Every symbol declared in include/gfq.h (checked by tests/test_abi.py).
 EXPORTS = ["gfq_last_error", "gfq_version", "gfq_code_create", "gfq_code_destroy", "gfq_code_info",
@@ -39,7 +40,8 @@ class gfq_params(ctypes.Structure):
                 ("schedule", ctypes.c_int), ("max_iters", ctypes.c_int),
                 ("early_exit", ctypes.c_int), ("markov_T", ctypes.c_void_p),
                 ("src_pi0", ctypes.c_void_p), ("keep_messages", ctypes.c_int),
-                ("trace_truth", ctypes.c_void_p), ("trace", ctypes.c_void_p)]
+                ("trace_truth", ctypes.c_void_p), ("trace", ctypes.c_void_p),
+                ("prior_update", ctypes.c_int)]
 
 
 class gfq_sim_params(ctypes.Structure):
@@ -120,7 +122,7 @@ class Params:
 
     def __init__(self, channel=GFQ_BSC, ch_param=0.0, schedule=GFQ_PUS, max_iters=100,
                  early_exit=True, markov_T=None, src_pi0=None, keep_messages=False,
-                 trace_truth=None, trace=None):
+                 trace_truth=None, trace=None, prior_update=GFQ_PRIOR_SNAPSHOT):
         """trace_truth / trace: CUDA tensors uint8 [F][N] and int32 [F][max_iters+1]
         (Fig. 1 instrumentation, see include/gfq.h), or None."""
         self._T = None if markov_T is None else np.ascontiguousarray(markov_T, dtype=np.float64)
@@ -130,7 +132,8 @@ class Params:
                             int(bool(early_exit)),
                             None if self._T is None else self._T.ctypes.data,
                             None if self._pi0 is None else self._pi0.ctypes.data,
-                            int(bool(keep_messages)), _dptr(trace_truth), _dptr(trace))
+                            int(bool(keep_messages)), _dptr(trace_truth), _dptr(trace),
+                            int(prior_update))
 
     def ref(self):
         return ctypes.byref(self.c)
