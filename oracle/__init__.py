@@ -60,7 +60,7 @@ def lib():
             L.o_unsatisfied.argtypes = [vp, vp, vp]
             L.o_unsatisfied.restype = i
             L.o_decode_frame.argtypes = [vp, i, i, i, vp, vp, vp, vp, vp, P(i), vp, vp, vp,
-                                         P(ctypes.c_long), vp, vp, i]
+                                         P(ctypes.c_long), vp, vp, i, vp, i]
             L.o_markov_prior_one.argtypes = [i, vp, vp, vp, vp, vp]
             L.o_decode_frame.restype = i
             _lib = L
@@ -182,12 +182,14 @@ class OCode:
 
     def decode(self, hard, pi, schedule: int = PUS, max_iters: int = 100, fixed: bool = False,
                T=None, pi0=None, keep_messages: bool = False, threads: int = 0, s_true=None,
-               sus_gs: bool = False):
+               sus_gs: bool = False, sus_order=None):
         """Decode frames. hard uint8 [F][M*p], pi float64 [F][M*p] (fp32 values may be
         passed: they are widened exactly).  Returns dict(xhat [F][V], iters [F],
         zero_norms [F], and q/r [F][E][q], Q [F][V][q] if keep_messages; with the true
         sources s_true uint8 [F][N] also trace [F][max_iters+1], the correct source
-        bits of the estimate after each iteration (Fig. 1))."""
+        bits of the estimate after each iteration (Fig. 1)).  sus_order: int
+        [n][V], SUS sweep t visits columns sus_order[(t-1) % n] (reading A35); None =
+        index order (A7)."""
         hard = np.ascontiguousarray(hard, dtype=np.uint8)
         pi = np.ascontiguousarray(pi, dtype=np.float64)
         F = hard.shape[0]
@@ -202,6 +204,10 @@ class OCode:
         p0 = None if pi0 is None else np.ascontiguousarray(pi0, dtype=np.float64)
         st = None if s_true is None else np.ascontiguousarray(s_true, dtype=np.uint8).reshape(F, self.N)
         tr = None if s_true is None else np.zeros((F, max(int(max_iters), 0) + 1), np.int32)
+        od = None if sus_order is None else np.ascontiguousarray(sus_order, dtype=np.int32).reshape(-1, V)
+        if od is not None:
+            assert not sus_gs, "sus_order is not combined with the in-sweep prior"
+            assert all(np.array_equal(np.sort(o), np.arange(V)) for o in od), "each order must permute 0..V-1"
         L = lib()
 
         def one(f):
@@ -213,7 +219,7 @@ class OCode:
                              _p(rm[f]) if keep_messages else None,
                              _p(Qm[f]) if keep_messages else None, ctypes.byref(z),
                              None if st is None else _p(st[f]), None if tr is None else _p(tr[f]),
-                             int(bool(sus_gs)))
+                             int(bool(sus_gs)), _p(od), 0 if od is None else len(od))
             iters[f] = it.value
             zn[f] = z.value
 

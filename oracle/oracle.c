@@ -404,12 +404,17 @@ static int correct_source_bits(int p, int N, const uint8_t *x, const uint8_t *s)
  *          posterior of j-1 computed earlier in THIS sweep and the posterior of
  *          j+1 from the previous sweep (none at t = 1: right factor 1); no
  *          post-iteration refresh.  0: the post-iteration snapshot (A9).
+ *   order, n_orders: SUS column order (reading A35): sweep t visits
+ *          the columns order[((t-1) mod n_orders)*V + k], k = 0..V-1 (each a
+ *          permutation of 0..V-1, drawn by the caller); NULL = index order (A7).
+ *          Not combined with sus_gs (its "j-1 of this sweep" assumes index order).
  */
 int o_decode_frame(const ocode *c, int schedule, int max_iters, int fixed,
                    const uint8_t *hard, const double *pi, const double *T,
                    const double *pi0_in, uint8_t *xhat, int *iters,
                    double *qmsg_out, double *rmsg_out, double *Q_out,
-                   long *zero_norms, const uint8_t *s_true, int *trace, int sus_gs)
+                   long *zero_norms, const uint8_t *s_true, int *trace, int sus_gs,
+                   const int *order, int n_orders)
 {
     const int p = c->p, q = c->q, N = c->N, M = c->M, V = c->V;
     const long E = c->E;
@@ -478,11 +483,13 @@ int o_decode_frame(const ocode *c, int schedule, int max_iters, int fixed,
             for (long e = 0; e < E; ++e)
                 zn += var_edge(c, e, prior + (size_t)c->edge_col[e] * q, rmsg, qmsg + (size_t)e * q);
         } else {
-            /* SUS: for each column j in index order (A7):
+            /* SUS: for each column j in index order (A7) or the given order (A35):
              * step 1: partial horizontal pass, r_ij for all i in column j, from the current q's;
              * step 2: partial vertical pass over column j. */
             if (gs && t > 1) memcpy(Qprev, Q, sizeof(double) * (size_t)V * q);
-            for (int j = 0; j < V; ++j) {
+            const int *ord = (order && n_orders > 0) ? order + (size_t)((t - 1) % n_orders) * V : NULL;
+            for (int k = 0; k < V; ++k) {
+                const int j = ord ? ord[k] : k;
                 for (int e = c->col_ptr[j]; e < c->col_ptr[j + 1]; ++e)
                     check_edge(c, e, z, qmsg, scratch_q, scratch_h, rmsg + (size_t)e * q);
                 if (gs && j < N) /* within-sweep prior (A34) */

@@ -687,3 +687,97 @@ def test_within_sweep_prior_reduces_to_iid_for_memoryless_T():
                   sus_gs=True)
     b = oc.decode(hard, pi, schedule=oracle.SUS, max_iters=4, fixed=True, pi0=row, keep_messages=True)
     assert np.max(np.abs(a["Q"] - b["Q"])) < 1e-12 and np.array_equal(a["iters"], b["iters"])
+
+
+# ----------------------------------------------------------------------------- SUS column order (f2, A35)
+@pytest.mark.parametrize("z", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_sus_order_reversed_fresh_read_closed_form(z):
+    """The sweep visits the columns in the given order (P:198-216 with the order of
+    reading A35): on the chain x0 - c0 - x1 - c1 - x2 visited 2, 1, 0, ONE sweep gives
+    x0 the exact marginal p0(a) p1(z0+a) p2(z0+z1+a), while x2 (visited first) has
+    only p2(a) p1(z1+a) -- the mirror image of the index-order closed form."""
+    oc = chain_code()
+    pi0 = np.array([0.3, 0.7])
+    p1, p2 = 0.2, 0.4
+    hard = np.array([[z[0], z[0] ^ z[1]]], np.uint8)
+    pi = np.array([[p1, p2]])
+    pr0, pr1, pr2 = pi0, np.array([1 - p1, p1]), np.array([1 - p2, p2])
+    z0, z1 = z
+    exact0 = np.array([pr0[a] * pr1[z0 ^ a] * pr2[z0 ^ z1 ^ a] for a in range(2)])
+    first2 = np.array([pr2[a] * pr1[z1 ^ a] for a in range(2)])
+    out = oc.decode(hard, pi, schedule=oracle.SUS, max_iters=1, fixed=True, pi0=pi0, keep_messages=True,
+                    sus_order=np.array([[2, 1, 0]]))
+    assert np.allclose(out["Q"][0, 0], exact0 / exact0.sum(), atol=1e-15)
+    assert np.allclose(out["Q"][0, 2], first2 / first2.sum(), atol=1e-15)
+    # index order: x0 first, so after one sweep it lacks x2's evidence
+    nat = oc.decode(hard, pi, schedule=oracle.SUS, max_iters=1, fixed=True, pi0=pi0, keep_messages=True)
+    lack = np.array([pr0[a] * pr1[z0 ^ a] for a in range(2)])
+    assert np.allclose(nat["Q"][0, 0], lack / lack.sum(), atol=1e-15)
+
+
+def test_sus_order_identity_is_index_order():
+    c = synth.CONFIGS["C1"]
+    code = synth.code_for(c)
+    fr = synth.frames_for(c, code, range(3))
+    oc = oracle.OCode.from_synth(code)
+    hard, pi = oracle.frontend(fr.channel, fr.ch_param, fr.obs)
+    a = oc.decode(hard, pi, schedule=oracle.SUS, max_iters=4, fixed=True, keep_messages=True)
+    b = oc.decode(hard, pi, schedule=oracle.SUS, max_iters=4, fixed=True, keep_messages=True,
+                  sus_order=np.arange(code.V)[None])
+    for k in ("q", "r", "Q"):
+        assert np.array_equal(a[k], b[k])
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_sus_order_tree_exactness(p):
+    """On cycle-free H, SUS with a different random column order every sweep still
+    reaches the brute-force marginals (BP is exact on trees under any schedule)."""
+    rng = np.random.default_rng(70 + p)
+    q = 1 << p
+    done = 0
+    while done < 6:
+        M = int(rng.integers(2, 5))
+        tc = random_tree_code(rng, M, q)
+        if tc is None:
+            continue
+        N, rows, cols, vals = tc
+        if N + M > (10 if p == 1 else 7):
+            continue
+        oc, hard, pi, z = setup_frame(rng, p, N, M, rows, cols, vals)
+        pi0 = rng.random(q)
+        pi0 /= pi0.sum()
+        priors = [pi0] * N + [oracle.noise_prior(p, pi[k * p:(k + 1) * p]) for k in range(M)]
+        want = brute_marginals(p, N, M, rows, cols, vals, z, priors)
+        orders = np.stack([rng.permutation(N + M) for _ in range(3)])
+        out = oc.decode(hard[None], pi[None], schedule=oracle.SUS, max_iters=2 * (N + M), fixed=True,
+                        pi0=pi0, keep_messages=True, threads=1, sus_order=orders)
+        assert np.max(np.abs(out["Q"][0] - want)) < 1e-9
+        done += 1
+
+
+def test_sus_order_fixed_points_agree_with_pus():
+    """A fixed point does not depend on the schedule: SUS in random orders and PUS agree."""
+    rng = np.random.default_rng(15)
+    agreed = 0
+    for trial in range(20):
+        p, N, M = 2, 3, 5
+        q = 1 << p
+        rows, cols = [], []
+        for j in range(N + M):
+            for i in rng.choice(M, 2, replace=False):
+                rows.append(i); cols.append(j)
+        rows = np.array(rows, np.int32)
+        cols = np.array(cols, np.int32)
+        vals = rng.integers(1, q, len(rows)).astype(np.uint8)
+        oc, hard, pi, z = setup_frame(rng, p, N, M, rows, cols, vals)
+        pi *= 0.3
+        orders = np.stack([rng.permutation(N + M) for _ in range(5)])
+        res = []
+        for kw in (dict(schedule=oracle.PUS), dict(schedule=oracle.SUS, sus_order=orders)):
+            o1 = oc.decode(hard[None], pi[None], max_iters=400, fixed=True, keep_messages=True, **kw)
+            o2 = oc.decode(hard[None], pi[None], max_iters=405, fixed=True, keep_messages=True, **kw)
+            res.append((np.max(np.abs(o1["Q"] - o2["Q"])) < 1e-13, o1["Q"][0]))
+        if res[0][0] and res[1][0]:
+            assert np.max(np.abs(res[0][1] - res[1][1])) < 1e-9
+            agreed += 1
+    assert agreed >= 5
