@@ -102,6 +102,17 @@ typedef struct {
      *     sweep runs about N dependency levels instead of ~13.
      * GFQ_EINVAL for other values or GFQ_PRIOR_IN_SWEEP with PUS. */
     int prior_update;
+    /* SUS column order (reading A35), host: sus_n_orders >= 1
+     * permutations of 0..N+M-1, row-major [sus_n_orders][N+M]; sweep t
+     * (1-based) visits the columns in row (t-1) mod sus_n_orders (P:198-216
+     * with that order in place of the index order).  NULL / 0 = index order
+     * (A7).  Random numbers the order is drawn from are the caller's.  The
+     * dependency levels of every order are built on the host per call and
+     * copied into the workspace (size it with the same params).  GFQ_EINVAL
+     * if a row is not a permutation, with PUS (whose updates do not depend on
+     * any order, A6) or with GFQ_PRIOR_IN_SWEEP (defined along index order). */
+    const int *sus_order;
+    int sus_n_orders;
 } gfq_params;
 
 /* Thread-local description of the last error (never NULL). */

@@ -53,6 +53,52 @@ struct GF {
   int inv(int x) const { return exp[(q - 1 - log[x]) % (q - 1)]; }
 };
 
+// SUS dependency levels for the sweep that visits the columns
+// in `order` (a permutation of 0..V-1; NULL = index order, A7): in the sweep
+// column j reads the q's of the other columns of its checks (and, with
+// chain = true -- the in-sweep Markov prior, A34 -- the posterior of source
+// column j-1).  level(j) = 1 + max level of the columns visited before j that
+// it depends on; columns of one level share no check, so running a level's
+// columns concurrently, levels in order, reads exactly what the serial sweep
+// reads.  Outputs: level_ptr [nlev+1], and the task tables in level order.
+int build_levels(const HostGraph &g, const int *order, bool chain, std::vector<int> &level_ptr,
+                 std::vector<LvlCol> &lcol, std::vector<LvlUnit> &lunit) {
+  const int V = g.V, N = g.N;
+  std::vector<int> lvl(V, 0), rowlvl(g.M, 0);
+  int nlev = 0;
+  for (int k = 0; k < V; ++k) {
+    const int j = order ? order[k] : k;
+    int L = (chain && j > 0 && j < N) ? lvl[j - 1] : 0;
+    for (int x = g.col_ptr[j]; x < g.col_ptr[j + 1]; ++x) L = std::max(L, rowlvl[g.edge_check[g.col_edge[x]]]);
+    L += 1;
+    lvl[j] = L;
+    for (int x = g.col_ptr[j]; x < g.col_ptr[j + 1]; ++x) rowlvl[g.edge_check[g.col_edge[x]]] = L;
+    nlev = std::max(nlev, L);
+  }
+  level_ptr.assign(nlev + 1, 0);
+  for (int j = 0; j < V; ++j) level_ptr[lvl[j]]++;  // lvl in 1..nlev -> slot lvl
+  for (int L = 0; L < nlev; ++L) level_ptr[L + 1] += level_ptr[L];
+  std::vector<int> cols(V), fill(level_ptr.begin(), level_ptr.end() - 1);
+  for (int k = 0; k < V; ++k) {  // within a level: visiting order
+    const int j = order ? order[k] : k;
+    cols[fill[lvl[j] - 1]++] = j;
+  }
+  lcol.resize(V);
+  lunit.clear();
+  lunit.reserve((size_t)g.E + V);
+  for (int k = 0; k < V; ++k) {
+    const int j = cols[k];
+    const int e0 = g.col_ptr[j], dv = g.col_ptr[j + 1] - e0;
+    lcol[k] = LvlCol{j, e0, dv, (int)lunit.size()};
+    if (dv == 0) lunit.push_back(LvlUnit{0, 0, 0, 0});
+    for (int s = 0; s < dv; ++s) {
+      const int e = g.col_edge[e0 + s], i = g.edge_check[e];
+      lunit.push_back(LvlUnit{g.row_ptr[i], g.row_ptr[i + 1] - g.row_ptr[i], e - g.row_ptr[i], i});
+    }
+  }
+  return nlev;
+}
+
 }  // namespace gfq
 
 using namespace gfq;
@@ -141,38 +187,14 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
     return GFQ_EUNSUPPORTED;
   }
 
-  // SUS dependency levels: in the
-  // sweep j = 0..V-1 (order A7) column j reads the q's of the other
-  // columns of its checks.  level(j) = 1 + max level of the earlier columns
-  // sharing a check with j; columns of one level share no check, so running a
-  // level's columns concurrently, levels in order, reads exactly the values
-  // the serial sweep reads.
-  // With the Markov prior refreshed inside the sweep (GFQ_PRIOR_IN_SWEEP,
-  // reading A34) source column j also reads the posterior of column j-1 of
-  // the same sweep: chain = true adds that dependency (level(j) > level(j-1)
-  // for 0 < j < N).
-  auto levels = [&](bool chain, std::vector<int> &level_ptr, std::vector<int> &level_cols) {
-    std::vector<int> lvl(V, 0), rowlvl(M, 0);
-    int nlev = 0;
-    for (int j = 0; j < V; ++j) {
-      int L = (chain && j > 0 && j < N) ? lvl[j - 1] : 0;
-      for (int k = col_ptr[j]; k < col_ptr[j + 1]; ++k) L = std::max(L, rowlvl[edge_check[col_edge[k]]]);
-      L += 1;
-      lvl[j] = L;
-      for (int k = col_ptr[j]; k < col_ptr[j + 1]; ++k) rowlvl[edge_check[col_edge[k]]] = L;
-      nlev = std::max(nlev, L);
-    }
-    level_ptr.assign(nlev + 1, 0);
-    level_cols.assign(V, 0);
-    for (int j = 0; j < V; ++j) level_ptr[lvl[j]]++;      // lvl in 1..nlev -> slot lvl
-    for (int L = 0; L < nlev; ++L) level_ptr[L + 1] += level_ptr[L];
-    std::vector<int> fill(level_ptr.begin(), level_ptr.end() - 1);
-    for (int j = 0; j < V; ++j) level_cols[fill[lvl[j] - 1]++] = j;
-    return nlev;
-  };
-  std::vector<int> level_ptr, level_cols, level_ptr_gs, level_cols_gs;
-  const int nlev = levels(false, level_ptr, level_cols);
-  const int nlev_gs = levels(true, level_ptr_gs, level_cols_gs);
+  // SUS dependency levels in index order (A7), without and with the in-sweep
+  // prior chain (A34); build_levels below
+  HostGraph hg{N, M, V, E, row_ptr, col_ptr, col_edge, edge_check};
+  std::vector<int> level_ptr, level_ptr_gs;
+  std::vector<LvlCol> lcol, lcol_gs;
+  std::vector<LvlUnit> lunit, lunit_gs;
+  const int nlev = build_levels(hg, nullptr, false, level_ptr, lcol, lunit);
+  const int nlev_gs = build_levels(hg, nullptr, true, level_ptr_gs, lcol_gs, lunit_gs);
 
   // static task tables (see gfq_internal.cuh)
   std::vector<CheckDesc> cdesc(M);
@@ -195,25 +217,6 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
       if (k != e) sdesc[cpos].perm_o[t++] = edge_perm[k];
     sdesc[cpos].perm_e = edge_perm[e];
   }
-  auto level_tables = [&](const std::vector<int> &cols, std::vector<LvlCol> &lcol, std::vector<LvlUnit> &lunit) {
-    lcol.resize(V);
-    lunit.clear();
-    lunit.reserve(E + V);
-    for (int k = 0; k < V; ++k) {
-      const int j = cols[k];
-      const int e0 = col_ptr[j], dv = col_ptr[j + 1] - e0;
-      lcol[k] = LvlCol{j, e0, dv, (int)lunit.size()};
-      if (dv == 0) lunit.push_back(LvlUnit{0, 0, 0, 0});
-      for (int s = 0; s < dv; ++s) {
-        const int e = col_edge[e0 + s], i = edge_check[e];
-        lunit.push_back(LvlUnit{row_ptr[i], row_ptr[i + 1] - row_ptr[i], e - row_ptr[i], i});
-      }
-    }
-  };
-  std::vector<LvlCol> lcol, lcol_gs;
-  std::vector<LvlUnit> lunit, lunit_gs;
-  level_tables(level_cols, lcol, lunit);
-  level_tables(level_cols_gs, lcol_gs, lunit_gs);
   const size_t U = lunit.size();
 
   // Encoder support (gfq_simulate, Eq. 1): an order that solves B t = y row by
@@ -291,8 +294,12 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   put(o_col, col_ptr.data(), sizeof(int) * (V + 1));
   put(o_cedge, col_edge.data(), sizeof(int) * E);
   put(o_canon, edge_canon.data(), sizeof(int) * E);
-  put(o_lptr, level_ptr.data(), sizeof(int) * (nlev + 1));
-  put(o_lcol, level_cols.data(), sizeof(int) * V);
+  {
+    std::vector<int> level_cols(V);
+    for (int k = 0; k < V; ++k) level_cols[k] = lcol[k].j;
+    put(o_lptr, level_ptr.data(), sizeof(int) * (nlev + 1));
+    put(o_lcol, level_cols.data(), sizeof(int) * V);
+  }
   put(o_mul, mul.data(), (size_t)q * q);
   put(o_rowtab, rowtab.data(), (size_t)q * q * 2);
   put(o_cdesc, cdesc.data(), sizeof(CheckDesc) * M);
@@ -319,6 +326,8 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
   c->p = p; c->q = q; c->N = N; c->M = M; c->V = V; c->poly = poly; c->E = E;
   c->max_cdeg = max_cdeg; c->max_vdeg = max_vdeg; c->n_levels = nlev; c->device = dev;
   c->level_ptr_h = level_ptr;
+  c->hg = std::move(hg);
+  c->n_units = (long long)U;
   c->n_levels_gs = nlev_gs;
   c->level_ptr_gs_h = level_ptr_gs;
   c->dev_blob = blob;

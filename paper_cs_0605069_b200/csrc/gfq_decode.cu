@@ -10,6 +10,7 @@
 //   then k_test (H x = z per frame) -> k_finalize -> k_capture
 //   (copy x of newly converged frames) -> k_compact (early exit: drop
 //   32-frame blocks whose frames all converged).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -51,6 +52,9 @@ Layout make_layout(const gfq_code *c, int fbw, const gfq_params *prm) {
   L.qs0 = markov ? take(qs) : kNone;
   L.qs1 = markov ? take(qs) : kNone;
   L.qall = prm->keep_messages ? take((size_t)c->V * c->q * F32 * sizeof(float)) : kNone;
+  const bool ord = prm->schedule == GFQ_SUS && prm->sus_order && prm->sus_n_orders > 0;
+  L.ord_col = ord ? take((size_t)prm->sus_n_orders * c->V * sizeof(LvlCol)) : kNone;
+  L.ord_unit = ord ? take((size_t)prm->sus_n_orders * c->n_units * sizeof(LvlUnit)) : kNone;
   L.iters = take(F32 * sizeof(int));
   L.conv = take(F32 * sizeof(int));
   L.unsat = take(F32 * sizeof(int));
@@ -93,6 +97,23 @@ static int check_params(const gfq_code *c, const gfq_params *prm, bool need_chan
   if (prm->prior_update == GFQ_PRIOR_IN_SWEEP && prm->schedule != GFQ_SUS) {
     set_error("prior_update = GFQ_PRIOR_IN_SWEEP needs schedule = GFQ_SUS (reading A34)");
     return GFQ_EINVAL;
+  }
+  if (prm->sus_order || prm->sus_n_orders) {
+    if (!prm->sus_order || prm->sus_n_orders < 1) { set_error("sus_order needs sus_n_orders >= 1"); return GFQ_EINVAL; }
+    if (prm->schedule != GFQ_SUS) { set_error("sus_order needs schedule = GFQ_SUS"); return GFQ_EINVAL; }
+    if (prm->prior_update == GFQ_PRIOR_IN_SWEEP) {
+      set_error("sus_order is not combined with GFQ_PRIOR_IN_SWEEP");
+      return GFQ_EINVAL;
+    }
+    std::vector<char> seen(c->V);
+    for (int o = 0; o < prm->sus_n_orders; ++o) {
+      std::fill(seen.begin(), seen.end(), 0);
+      const int *row = prm->sus_order + (size_t)o * c->V;
+      for (int k = 0; k < c->V; ++k) {
+        if (row[k] < 0 || row[k] >= c->V || seen[row[k]]) { set_error("sus_order row is not a permutation of 0..N+M-1"); return GFQ_EINVAL; }
+        seen[row[k]] = 1;
+      }
+    }
   }
   if ((prm->trace == nullptr) != (prm->trace_truth == nullptr)) {
     set_error("trace and trace_truth must both be set or both be NULL");
@@ -227,6 +248,29 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
   if (ce == cudaSuccess) ce = cudaMemsetAsync(at<unsigned long long>(ws, L.stats), 0, 4 * sizeof(unsigned long long), st);
   if (ce != cudaSuccess) return cuda_fail(ce, "upload decoder constants");
 
+  // level schedules of the caller's SUS column orders (A35), into the workspace
+  std::vector<std::vector<int>> ord_lptr;
+  const bool ordered = L.ord_col != kNone;
+  if (ordered) {
+    const int n = prm->sus_n_orders;
+    std::vector<LvlCol> hcol((size_t)n * c->V);
+    std::vector<LvlUnit> hunit((size_t)n * c->n_units);
+    ord_lptr.resize(n);
+    std::vector<LvlCol> lc;
+    std::vector<LvlUnit> lu;
+    for (int o = 0; o < n; ++o) {
+      build_levels(c->hg, prm->sus_order + (size_t)o * c->V, false, ord_lptr[o], lc, lu);
+      if ((long long)lu.size() != c->n_units) { set_error("internal: unit count"); return GFQ_EINVAL; }
+      std::copy(lc.begin(), lc.end(), hcol.begin() + (size_t)o * c->V);
+      std::copy(lu.begin(), lu.end(), hunit.begin() + (size_t)o * c->n_units);
+    }
+    ce = cudaMemcpyAsync(at<LvlCol>(ws, L.ord_col), hcol.data(), sizeof(LvlCol) * hcol.size(), cudaMemcpyHostToDevice, st);
+    if (ce == cudaSuccess)
+      ce = cudaMemcpyAsync(at<LvlUnit>(ws, L.ord_unit), hunit.data(), sizeof(LvlUnit) * hunit.size(), cudaMemcpyHostToDevice, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);  // host tables die at scope exit
+    if (ce != cudaSuccess) return cuda_fail(ce, "upload SUS order levels");
+  }
+
   const bool tracing = prm->trace != nullptr;
   const int tlen = prm->max_iters + 1;
   if (tracing) {
@@ -320,6 +364,16 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
       if (prm->schedule == GFQ_PUS) {
         RUN(K_CN, launch_cn(a, st));
         RUN(K_VN, launch_vn(a, st));
+      } else if (ordered) {  // sweep t in the caller's order (t-1) mod n (A35)
+        const int o = (t - 1) % prm->sus_n_orders;
+        WaveArgs ao = a;
+        ao.c.lvl_col = at<LvlCol>(ws, L.ord_col) + (size_t)o * c->V;
+        ao.c.lvl_unit = at<LvlUnit>(ws, L.ord_unit) + (size_t)o * c->n_units;
+        const std::vector<int> &op = ord_lptr[o];
+        for (int lv = 0; lv + 1 < (int)op.size(); ++lv) {
+          const int lb = op[lv], n = op[lv + 1] - lb;
+          if (n > 0) RUN(K_SUS, launch_sus_level(ao, lb, n, st));
+        }
       } else {
         for (int lv = 0; lv < nlev; ++lv) {
           const int lb = lptr[lv], n = lptr[lv + 1] - lb;

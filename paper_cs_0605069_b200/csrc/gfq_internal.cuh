@@ -45,6 +45,14 @@ struct __align__(16) LvlUnit {         // one per (column, check slot) in level 
 static_assert(sizeof(CheckDesc) == 128 && sizeof(VarDesc) == 64 && sizeof(SusDesc) == 64, "desc sizes");
 
 // -------------------------------------------------------------- code object
+struct HostGraph {             // host copy of the graph maps (level schedules per call)
+  int N, M, V;
+  long long E;
+  std::vector<int> row_ptr, col_ptr, col_edge, edge_check;
+};
+int build_levels(const HostGraph &g, const int *order, bool chain, std::vector<int> &level_ptr,
+                 std::vector<LvlCol> &lcol, std::vector<LvlUnit> &lunit);
+
 struct DevCode {
   int p, q, N, M, V;
   long long E;
@@ -83,6 +91,8 @@ struct gfq_code {
   std::vector<int> level_ptr_gs_h;
   const gfq::LvlCol *lvl_col_gs;    // device, same layout as DevCode::lvl_col
   const gfq::LvlUnit *lvl_unit_gs;
+  gfq::HostGraph hg;
+  long long n_units;                // U = sum over columns of max(dv, 1)
   void *dev_blob;  // one cudaMalloc holding every device table
   gfq::DevCode d;
 };
@@ -96,7 +106,7 @@ int cuda_fail(cudaError_t e, const char *what);
 struct Layout {
   int fbw;            // frame blocks per wave
   size_t qmsg, rmsg, pi, hard, z, xhat, qs0, qs1, qall, iters, conv, unsat, newconv;
-  size_t active, list, nactive, stats, T, Tf, pi0, total;
+  size_t active, list, nactive, stats, T, Tf, pi0, ord_col, ord_unit, total;
 };
 Layout make_layout(const gfq_code *c, int fbw, const gfq_params *prm);
 

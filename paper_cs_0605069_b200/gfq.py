@@ -41,7 +41,8 @@ class gfq_params(ctypes.Structure):
                 ("early_exit", ctypes.c_int), ("markov_T", ctypes.c_void_p),
                 ("src_pi0", ctypes.c_void_p), ("keep_messages", ctypes.c_int),
                 ("trace_truth", ctypes.c_void_p), ("trace", ctypes.c_void_p),
-                ("prior_update", ctypes.c_int)]
+                ("prior_update", ctypes.c_int), ("sus_order", ctypes.c_void_p),
+                ("sus_n_orders", ctypes.c_int)]
 
 
 class gfq_sim_params(ctypes.Structure):
@@ -122,18 +123,21 @@ class Params:
 
     def __init__(self, channel=GFQ_BSC, ch_param=0.0, schedule=GFQ_PUS, max_iters=100,
                  early_exit=True, markov_T=None, src_pi0=None, keep_messages=False,
-                 trace_truth=None, trace=None, prior_update=GFQ_PRIOR_SNAPSHOT):
+                 trace_truth=None, trace=None, prior_update=GFQ_PRIOR_SNAPSHOT, sus_order=None):
         """trace_truth / trace: CUDA tensors uint8 [F][N] and int32 [F][max_iters+1]
         (Fig. 1 instrumentation, see include/gfq.h), or None."""
         self._T = None if markov_T is None else np.ascontiguousarray(markov_T, dtype=np.float64)
         self._trace = (trace_truth, trace)
         self._pi0 = None if src_pi0 is None else np.ascontiguousarray(src_pi0, dtype=np.float64)
+        self._ord = None if sus_order is None else np.ascontiguousarray(np.atleast_2d(sus_order), dtype=np.int32)
         self.c = gfq_params(int(channel), float(ch_param), int(schedule), int(max_iters),
                             int(bool(early_exit)),
                             None if self._T is None else self._T.ctypes.data,
                             None if self._pi0 is None else self._pi0.ctypes.data,
                             int(bool(keep_messages)), _dptr(trace_truth), _dptr(trace),
-                            int(prior_update))
+                            int(prior_update),
+                            None if self._ord is None else self._ord.ctypes.data,
+                            0 if self._ord is None else int(self._ord.shape[0]))
 
     def ref(self):
         return ctypes.byref(self.c)
