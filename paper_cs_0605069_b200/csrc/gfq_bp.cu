@@ -74,6 +74,7 @@ struct KRof {
   static constexpr int v = Q <= 8 ? Q
                            : Q == 16 ? (K == KCN ? GFQ_KR_CN16 : K == KVN ? GFQ_KR_VN16 : GFQ_KR_SUS16)
                            : Q == 64 ? GFQ_KR64
+                           : Q == 128 ? 16   // KR^2 >= Q: the two register layouts cover every bit
                                      : 8;
 };
 // largest stage count in [2, max_s] such that the CTA fits the 227 KB of
@@ -102,11 +103,18 @@ struct PWof {
 #ifndef GFQ_G_T8_SUS
 #define GFQ_G_T8_SUS 2
 #endif
+// q = 128 (KR = 16, T = 8): one group per CTA so that a thread may use up to
+// 255 registers (16 fp64 entries of up to 4 messages)
 template <int T, int K = 0>
 struct Gof {
   static constexpr int g8 = K == KCN ? GFQ_G_T8_CN : K == KVN ? GFQ_G_T8_VN : GFQ_G_T8_SUS;
   static constexpr int v = T >= 8 ? g8 : (T >= 2 ? 2 : 4);
 };
+template <int Q, int T, int K>
+struct GQof {
+  static constexpr int v = Q >= 128 ? 1 : Gof<T, K>::v;
+};
+
 
 // ============================================================== PTX: mbarrier + TMA bulk copy
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -304,10 +312,14 @@ __device__ __forceinline__ void perm_addrs(uint32_t base, unsigned long long pk,
 template <int Q, int KR>
 __device__ __forceinline__ void tab_addrs(uint32_t base, const unsigned short *rowtab, unsigned long long pk, int c,
                                           uint32_t (&ad)[KR]) {
-  static_assert(KR == 2 || KR == 4 || KR == 8, "tab_addrs: KR");
+  static_assert(KR == 2 || KR == 4 || KR == 8 || KR == 16, "tab_addrs: KR");
   const unsigned short *p = rowtab + (size_t)(pk & 0xff) * Q + c * KR;
   uint32_t w[KR / 2];
-  if constexpr (KR == 8) {
+  if constexpr (KR == 16) {
+    const uint4 v = __ldg((const uint4 *)p), u = __ldg((const uint4 *)p + 1);
+    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+    w[4] = u.x; w[5] = u.y; w[6] = u.z; w[7] = u.w;
+  } else if constexpr (KR == 8) {
     const uint4 v = __ldg((const uint4 *)p);
     w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
   } else if constexpr (KR == 4) {
@@ -324,10 +336,13 @@ __device__ __forceinline__ void tab_addrs(uint32_t base, const unsigned short *r
 template <int Q, int KR>
 __device__ __forceinline__ void tab_addrs_sm(uint32_t base, uint32_t rt, unsigned long long pk, int c,
                                              uint32_t (&ad)[KR]) {
-  static_assert(KR == 2 || KR == 4 || KR == 8, "tab_addrs_sm: KR");
+  static_assert(KR == 2 || KR == 4 || KR == 8 || KR == 16, "tab_addrs_sm: KR");
   const uint32_t p = rt + (uint32_t)(((size_t)(pk & 0xff) * Q + c * KR) * 2);
-  uint32_t w[4];
-  if constexpr (KR == 8) {
+  uint32_t w[KR >= 8 ? KR / 2 : 4];
+  if constexpr (KR == 16) {
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(p));
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]) : "r"(p + 16));
+  } else if constexpr (KR == 8) {
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(p));
   } else if constexpr (KR == 4) {
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(p));
@@ -1659,6 +1674,7 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
     case 16: return F(16);    \
     case 32: return F(32);    \
     case 64: return F(64);    \
+    case 128: return F(128);  \
     default: break;           \
   }                           \
   set_error("unsupported q"); \
@@ -1692,7 +1708,7 @@ constexpr int stages_fit(int want) {
 
 template <int Q, int DM>
 static int cn_launch(const WaveArgs &a, cudaStream_t s) {
-  constexpr int KR = KRof<Q, KCN>::v, T = Q / KR, G = Gof<T, KCN>::v;
+  constexpr int KR = KRof<Q, KCN>::v, T = Q / KR, G = GQof<Q, T, KCN>::v;
   constexpr int NS = stages_fit<CNShape<Q, KR, DM, 1, G>, CNShape<Q, KR, DM, 2, G>>(Q == 16 ? GFQ_STAGES_Q16 : GFQ_STAGES_CN);
   using CS = CNShape<Q, KR, DM, NS, G>;
   if (CS::SMEM > 232448) return too_big("k_cn");
@@ -1709,7 +1725,10 @@ static int cn_q(const WaveArgs &a, cudaStream_t s) {
 
 template <int Q, int DV, bool MK>
 static int vn_launch(const WaveArgs &a, int clip, cudaStream_t s) {
-  constexpr int KR = KRof<Q, KVN>::v, T = Q / KR, G = Gof<T, KVN>::v;
+  if constexpr (Q >= 128 && MK) {
+    return too_big("k_vn (Markov prior, q = 128)");
+  } else {
+  constexpr int KR = KRof<Q, KVN>::v, T = Q / KR, G = GQof<Q, T, KVN>::v;
   constexpr int NS = stages_fit<VNShape<Q, KR, DV, MK, 1, G>, VNShape<Q, KR, DV, MK, 2, G>>(Q == 16 ? GFQ_STAGES_Q16 : GFQ_STAGES_VN);
   using VS = VNShape<Q, KR, DV, MK, NS, G>;
   if (VS::SMEM > 232448) return too_big("k_vn");
@@ -1717,6 +1736,7 @@ static int vn_launch(const WaveArgs &a, int clip, cudaStream_t s) {
   const int grid = grid_for(k, VS::THREADS, VS::SMEM, ((long long)a.nfb * a.c.V + G - 1) / G);
   k<<<grid, VS::THREADS, VS::SMEM, s>>>(a, clip);
   return check_launch("k_vn");
+  }
 }
 
 template <int Q>
@@ -1728,7 +1748,10 @@ static int vn_q(const WaveArgs &a, int clip, cudaStream_t s) {
 
 template <int Q, int DM, int DV, bool MK>
 static int sus_launch(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
-  constexpr int KR = KRof<Q, KSUS>::v, T = Q / KR, G = Gof<T, KSUS>::v;
+  if constexpr (Q >= 128 && MK) {
+    return too_big("k_sus (Markov prior, q = 128)");
+  } else {
+  constexpr int KR = KRof<Q, KSUS>::v, T = Q / KR, G = GQof<Q, T, KSUS>::v;
   constexpr int NS =
       stages_fit<SUSShape<Q, KR, DM, DV, MK, 1, G>, SUSShape<Q, KR, DM, DV, MK, 2, G>>(GFQ_STAGES_SUS);
   using SS = SUSShape<Q, KR, DM, DV, MK, NS, G>;
@@ -1751,6 +1774,7 @@ static int sus_launch(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
   cudaError_t e = cudaLaunchKernelEx(&cfg, k, a, lb, ncols);
   if (e != cudaSuccess) return cuda_fail(e, "k_sus");
   return check_launch("k_sus");
+  }
 }
 
 template <int Q>

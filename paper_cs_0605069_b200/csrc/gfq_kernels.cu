@@ -105,7 +105,7 @@ __global__ void k_init_msgs(WaveArgs a) {
     const int j = __ldg(a.c.edge_var + e);
     float *dst = a.qmsg + (size_t)w * q * 32 + lane;
     if (j >= N) {
-      double pb[6];
+      double pb[8];
       for (int b = 0; b < p; ++b) pb[b] = (double)a.pi[((size_t)fb * Mp + (size_t)(j - N) * p + b) * 32 + lane];
       for (int x = 0; x < q; ++x) {
         double v = 1.0;

@@ -31,7 +31,7 @@ def test_gf_field_axioms_exhaustive(p):
         assert sorted(mul[a, 1:]) == list(range(1, q))             # no zero divisors
 
 
-@pytest.mark.parametrize("p", [5, 6])
+@pytest.mark.parametrize("p", [5, 6, 7])
 def test_gf_large_fields_sampled(p):
     q = 1 << p
     rng = np.random.default_rng(p)
@@ -44,7 +44,7 @@ def test_gf_large_fields_sampled(p):
         assert oracle.gf_mul(a, oracle.gf_inv(a, p, POLY[p]), p, POLY[p]) == 1
 
 
-@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7])
 def test_gf_primitive_element_order(p):
     """x generates the multiplicative group: ord(x) = q-1 (the polynomials are primitive, A1)."""
     q = 1 << p
@@ -137,7 +137,8 @@ def brute_check(p, h, qin, z, out):
 
 
 @pytest.mark.parametrize("p,d", [(1, 1), (1, 2), (1, 3), (1, 4), (2, 2), (2, 3), (2, 4),
-                                 (3, 2), (3, 3), (3, 4), (4, 2), (4, 3), (6, 2), (6, 3)])
+                                 (3, 2), (3, 3), (3, 4), (4, 2), (4, 3), (6, 2), (6, 3),
+                                 (7, 2), (7, 3)])
 def test_check_node_equals_enumeration(p, d):
     q = 1 << p
     rng = np.random.default_rng(100 * p + d)
@@ -173,7 +174,7 @@ def test_check_node_q2_tanh_rule():
         assert abs((r[0] - r[1]) - pred) < 1e-13
 
 
-@pytest.mark.parametrize("p", [2, 3, 4, 6])
+@pytest.mark.parametrize("p", [2, 3, 4, 6, 7])
 def test_check_node_special_cases(p):
     q = 1 << p
     mul = synth.gf_tables(p).mul
