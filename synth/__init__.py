@@ -73,6 +73,8 @@ CONFIGS = {
                  (0.5, 1.0, 1.5, 2.0, 2.5, 3.0), 200),
     "C4": Config("C4", 4, 4, 8000, 16000, 8192, "markov", 0.9, BEC, (0.35,), 300),
     "C5": Config("C5", 5, 6, 10000, 20000, 8192, "iid", 0.0, BIAWGN, (1.5,), 400, 50),
+    # supplementary (not a BASELINE config): C5's construction over GF(128)
+    "X7": Config("X7", 6, 7, 10000, 20000, 4096, "iid", 0.0, BIAWGN, (1.5,), 400, 50),
 }
 
 
