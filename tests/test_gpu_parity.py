@@ -380,3 +380,41 @@ def test_low_degree_code_large_field_message_parity(gfq, p, markov):
         assert float(np.max(np.abs(rg.cpu().numpy() - ref["r"]))) <= MSG_TOL
         assert float(np.max(np.abs(Qg.cpu().numpy() - ref["Q"]))) <= MSG_TOL
         assert np.array_equal(it.cpu().numpy(), ref["iters"])
+
+
+def test_c5_bench_configuration_sampled(gfq):
+    """bench.py's workload and launch configuration: C5, 8192 frames from the
+    device front end (gfq_simulate, the bench's seed), fixed 50 iterations, PUS
+    in waves (workspace capped like bench.py) and SUS; four frames spread over
+    the batch (first and last wave, ragged ends of the waves' frame ranges)
+    recomputed one by one by the oracle from the same channel output."""
+    cfg = synth.CONFIGS["C5"]
+    code = synth.code_for(cfg)
+    gcode = gfq.Code.from_synth(code)
+    F, iters = cfg.frames, cfg.fixed_iters
+    sigma = synth.awgn_sigma(cfg.ch_params[0])
+    _, obs, _ = gfq.gfq_simulate(gcode, F, 0xBE7C0000 + cfg.cid * 64, gfq.GFQ_BIAWGN, sigma)
+    params = {s: gfq.Params(gfq.GFQ_BIAWGN, sigma, s, iters, early_exit=False) for s in (0, 1)}
+    torch.cuda.synchronize()
+    free, _ = torch.cuda.mem_get_info()
+    need = max(gfq.gfq_workspace_bytes(gcode, F, p) for p in params.values())
+    ws = gfq.alloc_workspace(int(min(need, free - (3 << 30))))
+    sample = np.array([0, 5119, 5120, F - 1])
+    oc = oracle.OCode.from_synth(code)
+    hard, pi = oracle.frontend(synth.BIAWGN, sigma, obs[torch.as_tensor(sample).cuda()].cpu().numpy())
+    s_hat = torch.empty((F, code.N), dtype=torch.uint8, device="cuda")
+    it = torch.empty(F, dtype=torch.int32, device="cuda")
+    for sched, prm in params.items():
+        gfq.gfq_decode(gcode, obs, prm, s_hat, it, ws)
+        torch.cuda.synchronize()
+        # the oracle may stop at the first passing iteration: in fixed-iteration mode the
+        # reported estimate and t are those of the first pass (DESIGN.md §4), and an
+        # i.i.d. source has no prior refresh that could differ afterwards
+        ref = oc.decode(hard, pi, schedule=sched, max_iters=iters)
+        got_x, got_it = s_hat.cpu().numpy()[sample], it.cpu().numpy()[sample]
+        print("C5 bench config", "PUS" if sched == 0 else "SUS", got_it, ref["iters"])
+        match, _ = _decision_match(got_x, got_it, ref["xhat"][:, :code.N], ref["iters"])
+        assert match.all()
+        assert gfq.gfq_decode_stats(gcode, ws)["zero_normalisers"] == 0
+    del ws
+    torch.cuda.empty_cache()

@@ -118,3 +118,21 @@ def test_sus_order_rejected_when_invalid(gfq):
         with pytest.raises(gfq.GfqError) as e:
             gfq.gfq_decode(gcode, torch.as_tensor(fr.obs).cuda(), prm)
         assert e.value.code == gfq.GFQ_EINVAL
+
+
+def test_sus_order_waves_and_ragged_frames(gfq):
+    """100 frames (ragged last block) through a workspace that holds 2 of the 4
+    32-frame blocks (2 waves): identical to one wave, and the order tables live
+    in every wave's workspace layout."""
+    cfg = synth.CONFIGS["C3"]
+    code = synth.code_for(cfg)
+    fr = synth.frames_for(cfg, code, range(100), point=3)
+    gcode = gfq.Code.from_synth(code)
+    orders = _orders(code.V, 4, 77)
+    prm = gfq.Params(gfq.GFQ_BIAWGN, fr.ch_param, gfq.GFQ_SUS, cfg.max_iters, sus_order=orders)
+    obs = torch.as_tensor(fr.obs).cuda()
+    s1, i1, _ = gfq.gfq_decode(gcode, obs, prm)
+    small = gfq.alloc_workspace(gfq.gfq_workspace_bytes(gcode, 64, prm))
+    s2, i2, _ = gfq.gfq_decode(gcode, obs, prm, workspace=small)
+    assert torch.equal(s1, s2) and torch.equal(i1, i2)
+    assert bool((i1 > 0).all())
