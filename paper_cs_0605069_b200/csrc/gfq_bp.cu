@@ -65,6 +65,9 @@ struct QC {
 #ifndef GFQ_KR_SUS16
 #define GFQ_KR_SUS16 8
 #endif
+#ifndef GFQ_ONEBAR_TMAX
+#define GFQ_ONEBAR_TMAX 4  // SUS variable-node reduction in one barrier up to this group size
+#endif
 enum KernelKind { KCN, KVN, KSUS };
 #ifndef GFQ_KR64
 #define GFQ_KR64 8
@@ -1632,7 +1635,7 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       if (last) {
         // vertical update of column j from the fresh r's (SUS step 2)
         group_bar<T>(g);  // rsm complete, transpose buffers free for the reduction
-#define SV(n) sus_vn<Q, KR, n, DVMAX, MARKOV, SS::PHASED && (T <= 4)>(a, hdr, xtra, sp.tsm, empty, rsm, SS::PHASED ? stage_x : red, g, c, lane, frozen, SS::PHASED, refill)
+#define SV(n) sus_vn<Q, KR, n, DVMAX, MARKOV, SS::PHASED && (T <= GFQ_ONEBAR_TMAX)>(a, hdr, xtra, sp.tsm, empty, rsm, SS::PHASED ? stage_x : red, g, c, lane, frozen, SS::PHASED, refill)
         switch (dv) {
           case 0: SV(0); break;
           case 1: SV(1); break;
