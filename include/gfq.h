@@ -42,8 +42,7 @@ extern "C" {
 #define GFQ_EINVAL (-1)       /* bad argument (see each call)                  */
 #define GFQ_ENOMEM (-2)       /* host or device allocation failed (create only) */
 #define GFQ_ECUDA (-3)        /* CUDA runtime error (message has the details)   */
-#define GFQ_EUNSUPPORTED (-4) /* valid but not implemented (p > 7, degree > 8,
-                                 Markov priors at p = 7: shared memory) */
+#define GFQ_EUNSUPPORTED (-4) /* valid but not implemented (p > 7, degree > 8)   */
 
 typedef enum { GFQ_BSC = 0, GFQ_BEC = 1, GFQ_BIAWGN = 2 } gfq_channel;
 typedef enum { GFQ_PUS = 0, GFQ_SUS = 1 } gfq_schedule;

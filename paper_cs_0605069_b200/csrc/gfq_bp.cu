@@ -1087,7 +1087,10 @@ struct VNShape {
   static constexpr bool ONEBAR = T > 1 && T <= 4;  // one-barrier reduction, red double-buffered
   static constexpr size_t RED_B = ((size_t)(DVMAX + 2) * T * 32 + (size_t)(DVMAX + 2) * 32 + T * 32) * 8;
   static constexpr size_t SCR = RED_B * (ONEBAR ? 2 : 1);
-  using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, MARKOV ? (size_t)2 * Q * Q * 4 : 0, false>;
+  // Markov T and T^T (fp32) in shared memory up to q = 64; at q = 128 (128 KB)
+  // they are read through L1 from the workspace copy
+  static constexpr bool TSMEM = MARKOV && Q <= 64;
+  using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, TSMEM ? (size_t)2 * Q * Q * 4 : 0, false>;
   static constexpr size_t SMEM = Sh::SMEM;
   static constexpr int THREADS = (G * T + (PWof<T>::v ? 1 : 0)) * 32;
 };
@@ -1140,10 +1143,11 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
   const SmemPtrs sp = smem_ptrs<Sh, S, G>(smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) init_bars<S, G>(sp.bars, T);
-  if constexpr (MARKOV) {
+  if constexpr (VS::TSMEM) {
     if (a.Tf)
       for (int k = threadIdx.x; k < 2 * Q * Q; k += blockDim.x) sp.tsm[k] = a.Tf[k];
   }
+  const float *Tp = VS::TSMEM ? sp.tsm : a.Tf;
   __syncthreads();
   const int V = a.c.V;
   const long long ntask = (long long)(*a.nactive) * V;
@@ -1191,7 +1195,7 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
     mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
     const int dv = ((const TaskInfo *)hdr)->deg;
     double *redt = VS::ONEBAR ? red + (size_t)(rr & 1) * (VS::RED_B / 8) : red;
-#define VT(n) vn_task<Q, KR, n, DVMAX, MARKOV>(a, hdr, pay, xtra, sp.tsm, empty, redt, g, c, lane, refill)
+#define VT(n) vn_task<Q, KR, n, DVMAX, MARKOV>(a, hdr, pay, xtra, Tp, empty, redt, g, c, lane, refill)
     switch (dv) {
       case 0: VT(0); break;
       case 1: VT(1); break;
@@ -1236,7 +1240,8 @@ struct SUSShape {
   static_assert(!PHASED || RED_D * 8 <= PAY, "reduction scratch must fit a stage payload");
   // shared region: Markov T and T^T (fp32), then the row-offset table (u16 q x q)
   // when it still fits (RTS; otherwise the table is read through L1)
-  static constexpr size_t TSM_F = MARKOV ? (size_t)2 * Q * Q : 0;
+  static constexpr bool TSMEM = MARKOV && Q <= 64;  // as VNShape
+  static constexpr size_t TSM_F = TSMEM ? (size_t)2 * Q * Q : 0;
   using Sh0 = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, TSM_F * 4, false>;
   static constexpr bool RTS = Sh0::SMEM + (size_t)2 * Q * Q <= 232448;
   using Sh = Shape<Q, S, G, PAY, SCR, (size_t)XR * 128, TSM_F * 4 + (RTS ? (size_t)2 * Q * Q : 0), false>;
@@ -1518,10 +1523,11 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
   // let the next level's CTAs start their prologue now; they wait below.
   asm volatile("griddepcontrol.launch_dependents;");
   if (threadIdx.x == 0) init_bars<S, G>(sp.bars, T);
-  if constexpr (MARKOV) {
+  if constexpr (SS::TSMEM) {
     if (a.Tf)
       for (int k = threadIdx.x; k < 2 * Q * Q; k += blockDim.x) sp.tsm[k] = a.Tf[k];
   }
+  const float *Tp = SS::TSMEM ? sp.tsm : a.Tf;
   unsigned short *rtab = (unsigned short *)(sp.tsm + SS::TSM_F);
   if constexpr (SS::RTS)
     for (int k = threadIdx.x; k < Q * Q; k += blockDim.x) rtab[k] = a.c.rowtab[k];
@@ -1635,7 +1641,7 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       if (last) {
         // vertical update of column j from the fresh r's (SUS step 2)
         group_bar<T>(g);  // rsm complete, transpose buffers free for the reduction
-#define SV(n) sus_vn<Q, KR, n, DVMAX, MARKOV, SS::PHASED && (T <= GFQ_ONEBAR_TMAX)>(a, hdr, xtra, sp.tsm, empty, rsm, SS::PHASED ? stage_x : red, g, c, lane, frozen, SS::PHASED, refill)
+#define SV(n) sus_vn<Q, KR, n, DVMAX, MARKOV, SS::PHASED && (T <= GFQ_ONEBAR_TMAX)>(a, hdr, xtra, Tp, empty, rsm, SS::PHASED ? stage_x : red, g, c, lane, frozen, SS::PHASED, refill)
         switch (dv) {
           case 0: SV(0); break;
           case 1: SV(1); break;
@@ -1728,9 +1734,7 @@ static int cn_q(const WaveArgs &a, cudaStream_t s) {
 
 template <int Q, int DV, bool MK>
 static int vn_launch(const WaveArgs &a, int clip, cudaStream_t s) {
-  if constexpr (Q >= 128 && MK) {
-    return too_big("k_vn (Markov prior, q = 128)");
-  } else {
+  {
   constexpr int KR = KRof<Q, KVN>::v, T = Q / KR, G = GQof<Q, T, KVN>::v;
   constexpr int NS = stages_fit<VNShape<Q, KR, DV, MK, 1, G>, VNShape<Q, KR, DV, MK, 2, G>>(Q == 16 ? GFQ_STAGES_Q16 : GFQ_STAGES_VN);
   using VS = VNShape<Q, KR, DV, MK, NS, G>;
@@ -1751,9 +1755,7 @@ static int vn_q(const WaveArgs &a, int clip, cudaStream_t s) {
 
 template <int Q, int DM, int DV, bool MK>
 static int sus_launch(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
-  if constexpr (Q >= 128 && MK) {
-    return too_big("k_sus (Markov prior, q = 128)");
-  } else {
+  {
   constexpr int KR = KRof<Q, KSUS>::v, T = Q / KR, G = GQof<Q, T, KSUS>::v;
   constexpr int NS =
       stages_fit<SUSShape<Q, KR, DM, DV, MK, 1, G>, SUSShape<Q, KR, DM, DV, MK, 2, G>>(GFQ_STAGES_SUS);

@@ -2,8 +2,8 @@
 16 entries per thread and 8 warps per q-vector (the two register layouts of
 the transform then cover all 7 bits), one group per CTA.  Parity against the
 oracle on a small MN code, both schedules, on the same seeded inputs and gates
-as tests/test_gpu_parity.py.  Markov priors at q = 128 do not fit shared memory
-and are rejected with GFQ_EUNSUPPORTED."""
+as tests/test_gpu_parity.py.  With a Markov source the q x q transition tiles
+(128 KB) are read through L1 instead of shared memory."""
 import numpy as np
 import pytest
 
@@ -69,13 +69,23 @@ def test_q128_decision_gate(gfq, code128, schedule):
     assert (it > 0).mean() > 0.5
 
 
-def test_q128_markov_unsupported(gfq, code128):
-    fr = _frames(code128, 4, 0.8)
+@pytest.mark.parametrize("schedule,prior", [(0, 0), (1, 0), (1, 1)], ids=["PUS", "SUS", "SUS-in-sweep"])
+def test_q128_markov_message_gate(gfq, code128, schedule, prior):
+    T = synth.markov_uniform_jump(128, 0.7)
+    fr = synth.make_frames(code128, 13, range(33), "markov", synth.BSC, 0.08, stay=0.7)
     gcode = gfq.Code.from_synth(code128)
-    prm = gfq.Params(gfq.GFQ_BIAWGN, fr.ch_param, 1, 5, markov_T=synth.markov_uniform_jump(128, 0.9))
-    with pytest.raises(gfq.GfqError) as e:
-        gfq.gfq_decode(gcode, torch.as_tensor(fr.obs).cuda(), prm)
-    assert e.value.code == gfq.GFQ_EUNSUPPORTED
+    prm = gfq.Params(gfq.GFQ_BSC, fr.ch_param, schedule, 5, early_exit=False, keep_messages=True, markov_T=T,
+                     prior_update=prior)
+    s_hat, it, ws = gfq.gfq_decode(gcode, torch.as_tensor(fr.obs).cuda(), prm)
+    qg, rg, Qg = (x.cpu().numpy() for x in gfq.gfq_export_messages(gcode, fr.F, ws, prm))
+    oc = oracle.OCode.from_synth(code128)
+    hard, pi = oracle.frontend(fr.channel, fr.ch_param, fr.obs)
+    ref = oc.decode(hard, pi, schedule=schedule, max_iters=5, fixed=True, keep_messages=True, T=T,
+                    sus_gs=bool(prior))
+    errs = {k: float(np.max(np.abs(g - ref[k]))) for k, g in (("q", qg), ("r", rg), ("Q", Qg))}
+    print("q=128 Markov", schedule, prior, errs)
+    assert max(errs.values()) <= MSG_TOL, errs
+    assert np.array_equal(it.cpu().numpy(), ref["iters"])
 
 
 def test_q128_simulate_then_decode(gfq, code128):
