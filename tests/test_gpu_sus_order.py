@@ -136,3 +136,21 @@ def test_sus_order_waves_and_ragged_frames(gfq):
     s2, i2, _ = gfq.gfq_decode(gcode, obs, prm, workspace=small)
     assert torch.equal(s1, s2) and torch.equal(i1, i2)
     assert bool((i1 > 0).all())
+
+
+def test_sus_order_zero_iterations_and_more_orders_than_sweeps(gfq):
+    """max_iters = 0 runs no sweep (clipped priors, iters -1) whatever the orders;
+    16 orders with 3 sweeps use only the first 3 (= a decode given those 3)."""
+    cfg = synth.CONFIGS["C1"]
+    code = synth.code_for(cfg)
+    fr = synth.frames_for(cfg, code, range(40))
+    gcode = gfq.Code.from_synth(code)
+    orders = _orders(code.V, 16, 99)
+    _, s0, i0, _ = _decode(gfq, gcode, fr, 0, False, None, orders)
+    _, s1, i1, _ = _decode(gfq, gcode, fr, 0, False, None, None)
+    assert np.array_equal(s0, s1) and (i0 == -1).all() and (i1 == -1).all()
+    prm, _, _, ws = _decode(gfq, gcode, fr, 3, False, None, orders, keep=True)
+    qa = gfq.gfq_export_messages(gcode, fr.F, ws, prm)[0].cpu().numpy()
+    prm, _, _, ws = _decode(gfq, gcode, fr, 3, False, None, orders[:3], keep=True)
+    qb = gfq.gfq_export_messages(gcode, fr.F, ws, prm)[0].cpu().numpy()
+    assert np.array_equal(qa, qb)
