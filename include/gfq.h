@@ -1,6 +1,6 @@
 /*
  * gfq.h -- C ABI of libgfq: batched belief-propagation decoding of
- * MacKay-Neal codes over GF(2^p) (q = 2^p = 2..64) on one NVIDIA B200.
+ * MacKay-Neal codes over GF(2^p) (q = 2^p = 2..128) on one NVIDIA B200.
  *
  * Method: Yacov, Efraim, Kfir, Kanter, Shental, "Parallel vs. Sequential
  * Belief Propagation Decoding of LDPC Codes over GF(q) and Markov Sources"
