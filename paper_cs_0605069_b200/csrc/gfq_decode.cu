@@ -267,7 +267,8 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
     ce = cudaMemcpyAsync(at<LvlCol>(ws, L.ord_col), hcol.data(), sizeof(LvlCol) * hcol.size(), cudaMemcpyHostToDevice, st);
     if (ce == cudaSuccess)
       ce = cudaMemcpyAsync(at<LvlUnit>(ws, L.ord_unit), hunit.data(), sizeof(LvlUnit) * hunit.size(), cudaMemcpyHostToDevice, st);
-    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);  // host tables die at scope exit
+    // pageable H2D copies are staged before cudaMemcpyAsync returns, so the host
+    // tables may die at scope exit (as hbuf above)
     if (ce != cudaSuccess) return cuda_fail(ce, "upload SUS order levels");
   }
 

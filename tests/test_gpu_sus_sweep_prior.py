@@ -138,3 +138,20 @@ def test_in_sweep_prior_rejected_for_pus_and_bad_values(gfq):
         with pytest.raises(gfq.GfqError) as e:
             gfq.gfq_decode(gcode, torch.as_tensor(fr.obs).cuda(), prm)
         assert e.value.code == gfq.GFQ_EINVAL
+
+
+def test_in_sweep_prior_waves_and_ragged_frames(gfq):
+    """70 frames (ragged) through a workspace for one 32-frame block (3 waves):
+    identical to a single wave (the posterior snapshots are per wave)."""
+    cfg = synth.CONFIGS["C2"]
+    code = synth.code_for(cfg)
+    fr = synth.make_frames(code, cfg.cid, range(70), "markov", synth.BSC, 0.12, stay=cfg.stay, point=5)
+    T = synth.markov_T_for(cfg)
+    gcode = gfq.Code.from_synth(code)
+    prm = gfq.Params(gfq.GFQ_BSC, fr.ch_param, gfq.GFQ_SUS, cfg.max_iters, markov_T=T, prior_update=1)
+    obs = torch.as_tensor(fr.obs).cuda()
+    s1, i1, _ = gfq.gfq_decode(gcode, obs, prm)
+    small = gfq.alloc_workspace(gfq.gfq_workspace_bytes(gcode, 32, prm))
+    s2, i2, _ = gfq.gfq_decode(gcode, obs, prm, workspace=small)
+    assert torch.equal(s1, s2) and torch.equal(i1, i2)
+    assert bool((i1 > 0).float().mean() > 0.9)
