@@ -345,7 +345,12 @@ def main():
         its = {}
         for s in schedules:
             pc = gfq.Params(ch, fr.ch_param, s, cfg.max_iters, early_exit=True, markov_T=T)
-            sh, ic, _ = gfq.gfq_decode(gcode, obs_c, pc, workspace=ws)
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            sh, ic, _ = gfq.gfq_decode(gcode, obs_c, pc, workspace=ws, stream=stream)
+            c1.record(stream)
+            torch.cuda.synchronize()
+            its[("ms", s)] = c0.elapsed_time(c1)
             its[s] = ic.cpu().numpy()
             errs = (sh.cpu().numpy() != truth[:nf]).any(axis=1)
             its[("fer", s)] = float(errs.mean())
@@ -354,7 +359,8 @@ def main():
             name = "pus" if s == gfq.GFQ_PUS else "sus"
             ok = its[s] > 0
             conv[name] = dict(mean_iters=float(its[s][ok].mean()) if ok.any() else None,
-                              nonconverged=int((~ok).sum()), frame_error_rate=its[("fer", s)])
+                              nonconverged=int((~ok).sum()), frame_error_rate=its[("fer", s)],
+                              ms_to_converge=its[("ms", s)])
         if len(schedules) == 2:
             both = (its[schedules[0]] > 0) & (its[schedules[1]] > 0)
             if both.any():

@@ -508,6 +508,26 @@ __device__ __forceinline__ void prior_from(const WaveArgs &a, int j, int c, int 
   const float *exr = ex + Q * 32;  // rows of j+1 (slot 1)
 #pragma unroll
   for (int k = 0; k < KR; ++k) { L[k] = 0.0f; R[k] = 0.0f; }
+  if (a.tj) {
+    // T = alpha I + beta 1 1^T (stay / uniform jump, readings A12): the same
+    // sums in O(q) -- sum_x Q(x) T[x][b] = beta sum_x Q(x) + alpha Q(b), and
+    // sum_c T[b][c] Q(c) likewise (T symmetric)
+    const float al = a.tj_alpha, be = a.tj_beta;
+    if (nb & 1) {
+      float sl = 0.0f;
+#pragma unroll 8
+      for (int x = 0; x < Q; ++x) sl += exl[x * 32 + lane];
+#pragma unroll
+      for (int k = 0; k < KR; ++k) L[k] = fmaf(al, exl[(c * KR + k) * 32 + lane], be * sl);
+    }
+    if (nb & 2) {
+      float sr = 0.0f;
+#pragma unroll 8
+      for (int x = 0; x < Q; ++x) sr += exr[x * 32 + lane];
+#pragma unroll
+      for (int k = 0; k < KR; ++k) R[k] = fmaf(al, exr[(c * KR + k) * 32 + lane], be * sr);
+    }
+  } else {
   if (nb & 1) {
 #pragma unroll 4
     for (int x = 0; x < Q; ++x) {
@@ -525,6 +545,7 @@ __device__ __forceinline__ void prior_from(const WaveArgs &a, int j, int c, int 
 #pragma unroll
       for (int k = 0; k < KR; ++k) R[k] = fmaf(qv, trow[k], R[k]);
     }
+  }
   }
 #pragma unroll
   for (int k = 0; k < KR; ++k) {

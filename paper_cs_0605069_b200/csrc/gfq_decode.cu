@@ -325,6 +325,16 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
     a.pi0 = at<double>(ws, L.pi0);
     a.markov = prm->markov_T != nullptr;
     a.gs = a.markov && prm->schedule == GFQ_SUS && prm->prior_update == GFQ_PRIOR_IN_SWEEP;
+    if (a.markov) {  // stay / uniform-jump structure (every diagonal entry equal, every other equal)
+      const double d0 = prm->markov_T[0], o0 = q > 1 ? prm->markov_T[1] : 0.0;
+      bool tj = true;
+      for (int x = 0; x < q && tj; ++x)
+        for (int y = 0; y < q; ++y)
+          if (prm->markov_T[x * q + y] != (x == y ? d0 : o0)) { tj = false; break; }
+      a.tj = tj;
+      a.tj_alpha = (float)(d0 - o0);
+      a.tj_beta = (float)o0;
+    }
     if (a.gs) {  // the level schedule with the source chain (gfq_code.cu)
       a.c.lvl_col = c->lvl_col_gs;
       a.c.lvl_unit = c->lvl_unit_gs;

@@ -137,6 +137,8 @@ struct WaveArgs {
   const double *pi0;    // [q]
   int markov;
   int gs;               // SUS with the Markov prior refreshed inside the sweep (A34)
+  int tj;               // T = alpha I + beta 1 1^T exactly: O(q) prior sums
+  float tj_alpha, tj_beta;
   int t;                // current iteration (1-based)
   int early_exit;
 };
