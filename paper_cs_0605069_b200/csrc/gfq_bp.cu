@@ -90,12 +90,15 @@ constexpr int fit_stages(size_t per_stage, size_t other, int max_s) {
 // groups per CTA for a given number of warps per group
 // dedicated producer warp (small q: short tasks) vs one producer lane per
 // group (q = 64: keeps the CTA at 16 warps and 128 registers per thread)
+#ifndef GFQ_PW_T2
+#define GFQ_PW_T2 1
+#endif
 #ifndef GFQ_PW_T4
 #define GFQ_PW_T4 1
 #endif
 template <int T>
 struct PWof {
-  static constexpr bool v = (T == 2 || (T == 4 && GFQ_PW_T4));  // measured: in-group producers win for T = 1, 8
+  static constexpr bool v = ((T == 2 && GFQ_PW_T2) || (T == 4 && GFQ_PW_T4));  // measured: in-group producers win for T = 1, 8
 };
 #ifndef GFQ_G_T8_CN
 #define GFQ_G_T8_CN 2
