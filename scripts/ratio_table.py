@@ -61,7 +61,8 @@ if calibrate:
                  std_ratio=float(q.std()))
         print(json.dumps(r), flush=True)
     sys.exit(0)
-for name in ["C1", "C2", "C3", "C4", "C5"]:
+only = [a[len("--configs="):].split(",") for a in sys.argv if a.startswith("--configs=")]
+for name in (only[0] if only else ["C1", "C2", "C3", "C4", "C5"]):
     cfg = synth.CONFIGS[name]
     code = synth.code_for(cfg)
     gc = gfq.Code.from_synth(code)
@@ -74,8 +75,12 @@ for name in ["C1", "C2", "C3", "C4", "C5"]:
         res = {}
         for sch in (gfq.GFQ_PUS, gfq.GFQ_SUS):
             prm = gfq.Params(ch, fr.ch_param, sch, cfg.max_iters, early_exit=True, markov_T=T)
-            s, it, _ = gfq.gfq_decode(gc, obs, prm)
+            torch.cuda.empty_cache()
+            free, _ = torch.cuda.mem_get_info()    # large batches decode in waves (workspace capped)
+            ws = gfq.alloc_workspace(int(min(gfq.gfq_workspace_bytes(gc, F, prm), free - (3 << 30))))
+            s, it, _ = gfq.gfq_decode(gc, obs, prm, workspace=ws)
             it = it.cpu().numpy(); s = s.cpu().numpy()
+            del ws
             res[sch] = (it, (s != fr.s).any(axis=1), (s != fr.s).mean())
         tp, ts = res[0][0], res[1][0]
         both = (tp > 0) & (ts > 0)
