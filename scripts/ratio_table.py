@@ -80,7 +80,7 @@ for name in (only[0] if only else ["C1", "C2", "C3", "C4", "C5"]):
             ws = gfq.alloc_workspace(int(min(gfq.gfq_workspace_bytes(gc, F, prm), free - (3 << 30))))
             s, it, _ = gfq.gfq_decode(gc, obs, prm, workspace=ws)
             it = it.cpu().numpy(); s = s.cpu().numpy()
-            del ws
+            del ws, _
             res[sch] = (it, (s != fr.s).any(axis=1), (s != fr.s).mean())
         tp, ts = res[0][0], res[1][0]
         both = (tp > 0) & (ts > 0)
