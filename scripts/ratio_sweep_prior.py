@@ -39,17 +39,18 @@ for name, noise in ([] if time_only else POINTS):
     code = synth.code_for(cfg)
     gc = gfq.Code.from_synth(code)
     T = synth.markov_T_for(cfg)
+    F = min(nf, cfg.frames)
     if noise is None:
-        fr = synth.frames_for(cfg, code, range(nf))
+        fr = synth.frames_for(cfg, code, range(F))
     else:
-        fr = synth.make_frames(code, cfg.cid, range(nf), cfg.source, cfg.channel, noise, stay=cfg.stay, point=99)
+        fr = synth.make_frames(code, cfg.cid, range(F), cfg.source, cfg.channel, noise, stay=cfg.stay, point=99)
     ch = {synth.BSC: gfq.GFQ_BSC, synth.BEC: gfq.GFQ_BEC, synth.BIAWGN: gfq.GFQ_BIAWGN}[fr.channel]
     obs = torch.as_tensor(fr.obs).cuda()
     sp, tp = decode(gc, obs, ch, fr.ch_param, gfq.GFQ_PUS, 0, T, cfg.max_iters)
     ss, ts = decode(gc, obs, ch, fr.ch_param, gfq.GFQ_SUS, 0, T, cfg.max_iters)
     sg, tg = decode(gc, obs, ch, fr.ch_param, gfq.GFQ_SUS, 1, T, cfg.max_iters)
     row = dict(config=name + ("" if noise is None else "-near-threshold"), channel=synth.CHANNEL_NAMES[cfg.channel],
-               q=cfg.q, noise=fr.ch_param, frames=nf, nonconv_pus=int((tp < 0).sum()),
+               q=cfg.q, noise=fr.ch_param, frames=F, nonconv_pus=int((tp < 0).sum()),
                sus_snapshot=stats(tp, ts), sus_in_sweep=stats(tp, tg),
                ser_pus=float((sp != fr.s).mean()), ser_sus_snapshot=float((ss != fr.s).mean()),
                ser_sus_in_sweep=float((sg != fr.s).mean()))
