@@ -113,17 +113,22 @@ void o_check_node(int p, unsigned poly, int d, const int *h, const double *qin,
     int q = 1 << p;
     double *S = (double *)calloc((size_t)q, sizeof(double));
     double *T = (double *)calloc((size_t)q, sizeof(double));
+    int *hx = (int *)malloc(sizeof(int) * (size_t)q);
     S[0] = 1.0;
     for (int k = 0; k < d; ++k) {
         if (k == out) continue;
+        /* the field products h_ij' x for every x (integer work only: the
+         * floating-point sum below is the same, term for term and in order) */
+        for (int x = 0; x < q; ++x) hx[x] = o_gf_mul(h[k], x, p, poly);
         for (int y = 0; y < q; ++y) T[y] = 0.0;
         for (int y = 0; y < q; ++y)
             for (int x = 0; x < q; ++x)
-                T[y] += qin[k * q + x] * S[y ^ o_gf_mul(h[k], x, p, poly)];
+                T[y] += qin[k * q + x] * S[y ^ hx[x]];
         memcpy(S, T, sizeof(double) * (size_t)q);
     }
     for (int a = 0; a < q; ++a)
         r[a] = S[z ^ o_gf_mul(h[out], a, p, poly)];
+    free(hx);
     free(S);
     free(T);
 }
@@ -151,12 +156,15 @@ int o_var_node(int q, int dv, const double *prior, const double *rin, int out,
     return 0;
 }
 
-/* Tie tolerance of the clipping step (reading A17 in DESIGN.md). */
-#define O_TIE_REL 1e-5
+/* Tie tolerance of the clipping step (reading A17 in DESIGN.md): values that
+ * agree to fp64 round-off (relative 1e-12) are ties; anything farther apart is
+ * decided by the strict argmax.  Exact ties (BEC coset-uniform posteriors, an
+ * all-erased frame) come out of this sum at round-off scale only. */
+#define O_TIE_REL 1e-12
 
 /* Pseudo-posterior, Eq. (5): Q_j^a = alpha_j p_j^a prod_i r_ij^a,
  * then "clipping": x_j = the a maximising Q_j (ties -> smallest a, where
- * values within a relative O_TIE_REL of the maximum count as ties, A17).
+ * values within fp64 round-off, relative O_TIE_REL, of the maximum are ties, A17).
  * Returns x_j; *zero_norm set to 1 if the normaliser vanished (A19). */
 int o_posterior(int q, int dv, const double *prior, const double *rin,
                 double *Q, int *zero_norm)
@@ -175,7 +183,7 @@ int o_posterior(int q, int dv, const double *prior, const double *rin,
     } else {
         for (int a = 0; a < q; ++a) Q[a] /= s;
     }
-    /* ties -> smallest a; values equal up to round-off (relative O_TIE_REL) are ties */
+    /* ties -> smallest a; values equal up to fp64 round-off (relative O_TIE_REL) are ties */
     double mx = 0.0;
     for (int a = 0; a < q; ++a)
         if (Q[a] > mx) mx = Q[a];

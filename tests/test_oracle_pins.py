@@ -235,14 +235,56 @@ def test_var_node_properties():
 
 
 def test_posterior_clipping_ties_smallest():
-    """Reading A17: ties go to the smallest a; values within a relative 1e-5 of the
-    maximum are ties (round-off must not decide the clipping)."""
+    """Reading A17: clipping is the strict argmax; only values equal up
+    to fp64 round-off (relative 1e-12) are ties, and ties go to the smallest a."""
     Q, x, _ = oracle.posterior([0.25] * 4, [[0.1, 0.4, 0.4, 0.1]])
-    assert x == 1
+    assert x == 1                                   # exact tie -> smallest a
+    Q, x, _ = oracle.posterior([0.25] * 4, [[0.1, 0.4 * (1 - 1e-15), 0.4, 0.1]])
+    assert x == 1                                   # round-off tie
     Q, x, _ = oracle.posterior([0.25] * 4, [[0.1, 0.4 * (1 - 1e-7), 0.4, 0.1]])
-    assert x == 1
+    assert x == 2                                   # a genuine 1e-7 difference decides
     Q, x, _ = oracle.posterior([0.25] * 4, [[0.1, 0.4 * (1 - 1e-3), 0.4, 0.1]])
     assert x == 2
+
+
+def test_clipping_bec_coset_uniform_priors():
+    """BEC (reading A15): the prior of a noise symbol n_k is uniform over the coset
+    {n : n_b = 0 for every unerased bit b} (P:246-251 with flip probability 0 or
+    1/2 per bit) -- an exact tie among 2^(#erased bits) values that only the tie
+    rule resolves.  Clipping the priors (max_iters = 0) must give the
+    smallest member, n = 0, for every noise symbol (and 0 for the uniform
+    sources); a largest-a or round-off-decided rule gives other coset members."""
+    cfg = synth.CONFIGS["C4"]
+    code = synth.code_for(cfg)
+    fr = synth.frames_for(cfg, code, range(3))
+    oc = oracle.OCode.from_synth(code)
+    hard, pi = oracle.frontend(fr.channel, fr.ch_param, fr.obs)
+    out = oc.decode(hard, pi, max_iters=0, keep_messages=True)
+    p, N = code.p, code.N
+    n_erased = (fr.obs.reshape(3, code.M, p) == 2).sum(-1)           # [F][M]
+    Qn = out["Q"][:, N:, :]
+    ties = (Qn == Qn.max(-1, keepdims=True)).sum(-1)
+    assert np.array_equal(ties, 2 ** n_erased)                      # exact coset ties
+    assert (n_erased > 0).mean() > 0.5
+    assert (out["xhat"] == 0).all()
+
+
+def test_all_erased_frame_decodes_to_zero():
+    """A fully erased BEC frame: every hard bit is 0, so z = B 0 = 0, and every prior
+    and therefore every message and posterior is exactly uniform (q is a power of 2:
+    the sums of Eq. (3) are exact).  All q posterior values tie exactly, the tie rule
+    gives x = 0, which solves H x = 0 = z: the decoder stops at t = 1 with x = 0."""
+    cfg = synth.CONFIGS["C4"]
+    code = synth.code_for(cfg)
+    oc = oracle.OCode.from_synth(code)
+    obs = np.full((1, code.M * code.p), 2, np.uint8)
+    hard, pi = oracle.frontend(synth.BEC, 1.0, obs)
+    T = synth.markov_T_for(cfg)
+    for schedule in (oracle.PUS, oracle.SUS):
+        out = oc.decode(hard, pi, schedule=schedule, max_iters=3, T=T, keep_messages=True)
+        assert out["iters"][0] == 1
+        assert (out["xhat"] == 0).all()
+        assert np.all(out["Q"] == 1.0 / code.q)                          # exactly uniform
 
 
 # ----------------------------------------------------------------------------- Markov prior, Eqs. (6)/(7)
