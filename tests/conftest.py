@@ -44,3 +44,15 @@ def load_markov_golden():
 @pytest.fixture(scope="session")
 def golden():
     return load_golden()
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    """Print the decision-gate table (mismatches and tie-allowance counts) even under -q."""
+    try:
+        import gate
+    except ImportError:
+        return
+    if gate.GATE_LOG:
+        terminalreporter.write_sep("-", "decision gates (reading A18, tie allowance %g)" % gate.TIE_ALLOW)
+        for row in gate.GATE_LOG:
+            terminalreporter.write_line(row)

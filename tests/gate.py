@@ -1,0 +1,59 @@
+"""Decision-gate comparison (reading A18 + the fp32 tie allowance), shared by the
+GPU parity tests.  Comparison logic only: no arithmetic of the method lives here.
+
+A frame matches when
+  (i)  both decoders converge at the same iteration t with identical x_hat, or
+  (ii) neither converges within max_iters (A18: post-threshold chaos is not gated), or
+  (iii) both converge at the same t and every symbol where x_hat differs is one
+       where the GPU's choice is a near-tie of the ORACLE's posterior: Q_j(x_gpu)
+       >= (1 - TIE_ALLOW) max_a Q_j(a).  The oracle's clipping is the strict argmax
+       (ties only at fp64 round-off); the GPU stores messages in fp32,
+       so posteriors that differ by less than its storage error may clip to a
+       different symbol.  Frames matched this way are counted and reported.
+The gate requires matches on >= 99.9 % of frames (BASELINE.json north_star).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+TIE_ALLOW = 1e-5
+GATE_LOG: list = []   # rows printed by conftest.pytest_terminal_summary
+
+
+def decision_gate(gpu_x, gpu_it, ref_x, ref_it, oracle_Q_for=None):
+    """gpu_x/ref_x [F][n] symbols, gpu_it/ref_it [F].  oracle_Q_for(frame_idx) ->
+    (x [k][n], Q [k][n][q]): the oracle's final estimate and posterior for those
+    frames (only called for frames that converge at the same t with different x).
+    Returns (match [F] bool, strict [F] bool, n_allowance)."""
+    gpu_x, ref_x = np.asarray(gpu_x), np.asarray(ref_x)
+    gpu_it, ref_it = np.asarray(gpu_it), np.asarray(ref_it)
+    both_fail = (gpu_it == -1) & (ref_it == -1)
+    same_it = gpu_it == ref_it
+    eq = np.all(gpu_x == ref_x, axis=1)
+    strict = same_it & eq
+    match = both_fail | strict
+    cand = np.where(same_it & ~eq & ~both_fail)[0]
+    n_allow = 0
+    if len(cand) and oracle_Q_for is not None:
+        ox, oQ = oracle_Q_for(cand)
+        for k, f in enumerate(cand):
+            assert np.array_equal(ox[k], ref_x[f]), "oracle re-decode is not deterministic"
+            diff = np.where(gpu_x[f] != ref_x[f])[0]
+            Q = oQ[k][diff]
+            got = Q[np.arange(len(diff)), gpu_x[f][diff]]
+            if np.all(got >= Q.max(-1) * (1.0 - TIE_ALLOW)):
+                match[f] = True
+                n_allow += 1
+    return match, strict, n_allow
+
+
+def record(case: str, F: int, match, strict, n_allow, extra: str = "") -> int:
+    """Log one gate result; returns the number of mismatching frames."""
+    mism = int((~np.asarray(match)).sum())
+    GATE_LOG.append("%-34s frames %5d  mismatch %3d  strict-mismatch %3d  tie-allowance %3d  %s" % (
+        case, F, mism, int((~np.asarray(strict)).sum()), n_allow, extra))
+    return mism
+
+
+def allowed(F: int) -> int:
+    return int(np.floor(0.001 * F))

@@ -14,6 +14,7 @@ Gates as tests/test_gpu_parity.py."""
 import numpy as np
 import pytest
 
+import gate
 import oracle
 import synth
 
@@ -64,7 +65,12 @@ def test_paper_4state_source_with_stationary_pi0(gfq, schedule, prior):
     s, it, _ = gfq.gfq_decode(gcode, torch.as_tensor(fr.obs).cuda(), prm)
     ref = oc.decode(hard, pi, schedule=schedule, max_iters=150, T=T, pi0=pi0, sus_gs=bool(prior))
     s, it = s.cpu().numpy(), it.cpu().numpy()
-    ok = ((it == ref["iters"]) & np.all(s == ref["xhat"][:, :code.N], axis=1)) | ((it == -1) & (ref["iters"] == -1))
+    def oq(idx):
+        o = oc.decode(hard[idx], pi[idx], schedule=schedule, max_iters=150, T=T, pi0=pi0, sus_gs=bool(prior),
+                      keep_messages=True)
+        return o["xhat"][:, :code.N], o["Q"][:, :code.N]
+    ok, strict, n_allow = gate.decision_gate(s, it, ref["xhat"][:, :code.N], ref["iters"], oq)
+    gate.record("4S stationary %s prior %d" % ("SUS" if schedule else "PUS", prior), len(ok), ok, strict, n_allow)
     assert ok.all()
 
 
