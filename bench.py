@@ -12,7 +12,12 @@ GF(64), N=10000, M=20000, BI-AWGN 1.5 dB, 8192 frames, fixed 50 iterations
 value = decoded information bits per second over the whole job (all ranks):
 2 decodes x F x N x log2(q) bits per step per rank / max-over-ranks time.
 Multi-GPU: every rank decodes its own F frames (frames are independent, no
-collective on the data path) -> weak scaling.
+collective on the data path) -> weak scaling.  `--gpus N` without a torchrun
+environment re-runs itself under torch.distributed.run with N processes.
+The timed region runs with per-launch instrumentation OFF; one extra,
+instrumented step afterwards gives the per-kernel times of the roofline.
+`secondary` repeats the measurement on C4 (GF(16), BEC, Markov, 8192 frames,
+fixed 50 iterations; BASELINE.json configs[3]).
 `--impl reference` times the fp64 CPU oracle (oracle/) on a bounded sample of
 the same workload on this host's cores (the reference arm of this tier).
 """
@@ -51,6 +56,9 @@ def parse():
     ap.add_argument("--schedules", default="pus,sus")
     ap.add_argument("--host-gen", action="store_true",
                     help="generate the frames with the host generator synth/ instead of gfq_simulate")
+    ap.add_argument("--secondary", default="C4", help="second workload in the same line ('' = none)")
+    ap.add_argument("--secondary-steps", type=int, default=3)
+    ap.add_argument("--secondary-iters", type=int, default=50)
     return ap.parse_args()
 
 
@@ -200,51 +208,40 @@ def run_reference(args, cfg, iters, F):
     return 0
 
 
-def main():
-    args = parse()
-    cfg = synth.CONFIGS[args.config]
-    iters = args.iters or cfg.fixed_iters or cfg.max_iters
-    F = args.frames or cfg.frames
-    if args.impl == "reference":
-        return run_reference(args, cfg, iters, F)
+ARITH = {16: "q*r fp32 direct convolution (SUS), fp64 transforms (PUS), fp64 variable node; fp32 storage",
+         64: "fp64 registers (transforms, products, normalisation), fp32 message storage"}
 
+
+def decode_run(args, cfg, F, iters, schedules, steps, warmup, gfq, shard, dist, rank, world, local,
+               full=True):
+    """One workload: inputs on the device, `warmup` + `steps` clean timed steps through
+    shard.run_rank, one instrumented step for the per-kernel times, the roofline of
+    every hot kernel; with full=True also e2e, convergence and the CPU baseline."""
     import torch
-    import torch.distributed as dist
-    rank, world, local = dist_env()
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    import __graft_entry__
-    __graft_entry__.build()
-    from paper_cs_0605069_b200 import gfq, shard
-
-    schedules = [gfq.GFQ_PUS if s == "pus" else gfq.GFQ_SUS for s in args.schedules.split(",")]
     code = synth.code_for(cfg)
     gcode = gfq.Code.from_synth(code)
-    # rank r decodes frames [r*F, (r+1)*F) of the config's stream
     T = synth.markov_T_for(cfg)
     t_gen = time.perf_counter()
+    ids = shard.frame_range(rank, world, F)
+    param = cfg.ch_params[args.point if cfg.name == args.config else 0]
+    if cfg.channel == synth.BIAWGN:
+        param = synth.awgn_sigma(param)
+    ch = {synth.BSC: gfq.GFQ_BSC, synth.BEC: gfq.GFQ_BEC, synth.BIAWGN: gfq.GFQ_BIAWGN}[cfg.channel]
+    seed = 0xBE7C0000 + cfg.cid * 64 + (args.point if cfg.name == args.config else 0)
     if args.host_gen:
-        fr = synth.frames_for(cfg, code, shard.frame_range(rank, world, F), point=args.point)
+        fr = synth.frames_for(cfg, code, ids, point=args.point if cfg.name == args.config else 0)
         obs_host = torch.from_numpy(fr.obs).pin_memory()
         obs = obs_host.to("cuda", non_blocking=True)
         truth = fr.s
     else:
         # Monte-Carlo front end on the device (gfq_simulate, counter-based Philox
         # draws: the same frames for any rank count / subset)
-        param = cfg.ch_params[args.point]
-        if cfg.channel == synth.BIAWGN:
-            param = synth.awgn_sigma(param)
-        ch0 = {synth.BSC: gfq.GFQ_BSC, synth.BEC: gfq.GFQ_BEC, synth.BIAWGN: gfq.GFQ_BIAWGN}[cfg.channel]
-        s_dev, obs, _ = gfq.gfq_simulate(gcode, F, 0xBE7C0000 + cfg.cid * 64 + args.point, ch0, param,
-                                         frame0=shard.frame_range(rank, world, F)[0], markov_T=T)
+        s_dev, obs, _ = gfq.gfq_simulate(gcode, F, seed, ch, param, frame0=ids[0], markov_T=T)
         obs_host = obs.cpu().pin_memory()
         truth = s_dev.cpu().numpy()
-        fr = argparse.Namespace(channel=cfg.channel, ch_param=param, obs=None, s=truth)
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
-    ch = {synth.BSC: gfq.GFQ_BSC, synth.BEC: gfq.GFQ_BEC, synth.BIAWGN: gfq.GFQ_BIAWGN}[fr.channel]
-    params = {s: gfq.Params(ch, fr.ch_param, s, iters, early_exit=False, markov_T=T) for s in schedules}
+    params = {s: gfq.Params(ch, param, s, iters, early_exit=False, markov_T=T) for s in schedules}
     s_hat = torch.empty((F, cfg.N), dtype=torch.uint8, device="cuda")
     it = torch.empty(F, dtype=torch.int32, device="cuda")
     torch.cuda.synchronize()
@@ -254,152 +251,198 @@ def main():
     ws = gfq.alloc_workspace(ws_bytes)
     stream = torch.cuda.current_stream()
 
-    def step():
+    def step(_ids=None):
         for s in schedules:
             gfq.gfq_decode(gcode, obs, params[s], s_hat, it, ws, stream)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    def timer(fn):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
     clocks = ClockSampler(local)
-    clocks.start()
-    gfq.gfq_profile_enable(True)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
     gfq.gfq_profile_enable(False)
+    torch.cuda.synchronize()
+    clocks.start()
+    res = shard.run_rank(step, F, steps, warmup, lambda fn: timer(fn), dist=dist if world > 1 else None,
+                         device="cuda", last_iters=lambda: it.cpu().tolist())
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
+    ms = res.ms_max
+    # one instrumented step: per-kernel CUDA-event times (they break the
+    # programmatic-dependent-launch overlap of the SUS levels: a little slower)
+    gfq.gfq_profile_enable(True)
+    ms_prof = timer(step)
+    gfq.gfq_profile_enable(False)
     prof = gfq.gfq_profile_read()
     st = gfq.gfq_decode_stats(gcode, ws)
-    if world > 1:
-        ms = shard.max_over_ranks(ms, dist, device="cuda")   # the slowest rank's device time
-        dist.barrier()
+    launches_per_step = sum(n for _, n in prof.values())
     bits_per_step_rank = len(schedules) * F * cfg.N * cfg.p
-    value = bits_per_step_rank * world * args.steps / (ms / 1e3)
-    edge_updates = 2.0 * cfg.E * iters * F * len(schedules) * args.steps * world
-    launches_timed = sum(n for _, n in prof.values())
+    value = bits_per_step_rank * world * steps / (ms / 1e3)
+    edge_updates = 2.0 * cfg.E * iters * F * len(schedules) * steps * world
 
-    # roofline of the dominant kernel (8q bytes per edge-message update)
+    # roofline of every hot kernel (8q bytes per edge-message update)
     kinds = {k: v for k, v in prof.items() if v[1] > 0}
-    dom = max(kinds, key=lambda k: kinds[k][0])
-    dom_ms, dom_n = kinds[dom]
-    upd_per_frame_iter = {"cn": cfg.E, "vn": cfg.E, "sus": 2 * cfg.E}
-    alg_bytes = None
-    if dom in upd_per_frame_iter:
-        n_sched = sum(1 for s in schedules if (s == gfq.GFQ_SUS) == (dom == "sus"))
-        alg_bytes = 8.0 * cfg.q * upd_per_frame_iter[dom] * F * iters * n_sched * args.steps
     peak, peak_src = measured_peak()
-    roof = None
-    if alg_bytes is not None:
-        achieved = alg_bytes / (dom_ms / 1e3) / 1e9
-        traffic, traffic_src = None, None
-        import glob
+    upd_per_frame_iter = {"cn": cfg.E, "vn": cfg.E, "sus": 2 * cfg.E}
+    import glob
+    roofs = {}
+    for kname, (k_ms, k_n) in kinds.items():
+        if kname not in upd_per_frame_iter:
+            continue
+        n_sched = sum(1 for s in schedules if (s == gfq.GFQ_SUS) == (kname == "sus"))
+        alg = 8.0 * cfg.q * upd_per_frame_iter[kname] * F * iters * n_sched
+        traffic, tsrc = None, None
         for tpath in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_traffic.json")), reverse=True):
             try:
                 tj = json.load(open(tpath))
             except Exception:
                 continue
-            kk = tj.get("kernels", {}).get(dom)
+            kk = tj.get("kernels", {}).get(kname)
             if tj.get("config") == cfg.name and kk and kk.get("dram_per_alg_byte"):
-                # ncu dram__bytes_read+write of one captured launch, as bytes per algorithmic
-                # byte, applied to this run's average launch
-                traffic = kk["dram_per_alg_byte"] * alg_bytes / dom_n
-                traffic_src = os.path.relpath(tpath, ROOT)
+                traffic = kk["dram_per_alg_byte"] * alg / k_n     # ncu dram bytes per algorithmic byte x this launch
+                tsrc = os.path.relpath(tpath, ROOT)
                 break
-        roof = dict(bound="hbm", kernel=dom, achieved=achieved, peak=peak, unit="GB/s",
-                    frac=achieved / peak, traffic=traffic,
-                    alg_bytes_per_launch=alg_bytes / dom_n, launches=dom_n, traffic_source=traffic_src,
-                    avg_launch_ms=dom_ms / dom_n, peak_source=peak_src)
-    # whole-step model bandwidth (all kernels)
-    model_gbs = model_bytes_per_frame_iter(cfg) * F * iters * len(schedules) * args.steps / (ms / 1e3) / 1e9
+        achieved = alg / (k_ms / 1e3) / 1e9
+        roofs[kname] = dict(bound="hbm", kernel=kname, achieved=achieved, peak=peak, unit="GB/s",
+                            frac=achieved / peak, traffic=traffic, alg_bytes_per_launch=alg / k_n,
+                            launches=k_n, avg_launch_ms=k_ms / k_n, traffic_source=tsrc, peak_source=peak_src)
+    dom = max(roofs, key=lambda k: kinds[k][0]) if roofs else None
+    model_gbs = model_bytes_per_frame_iter(cfg) * F * iters * len(schedules) * steps / (ms / 1e3) / 1e9
+    out = dict(value=value, ms_per_step=ms / steps, ms_per_step_instrumented=ms_prof,
+               edge_msg_updates_per_s=edge_updates / (ms / 1e3), model_hbm_gbs=model_gbs,
+               roofline=roofs.get(dom), rooflines=roofs, clocks=clk,
+               gpu_launches=int(launches_per_step * steps),
+               kernels={k: dict(ms=v[0], launches=v[1]) for k, v in kinds.items()},
+               health=dict(zero_normalisers_last_decode=st["zero_normalisers"]),
+               config=dict(workload(cfg, F, iters), arith=ARITH.get(cfg.q, ARITH[64]),
+                           parallelism="frame-sharded dp%d (no collective)" % world,
+                           l2="inputs larger than L2 (message state %.1f GB/GPU vs 126 MB)" %
+                              (cfg.E * cfg.q * 4 * F * 2 / 1e9),
+                           timing="clean (no per-launch events); kernels from one extra instrumented step",
+                           workspace_gb=ws_bytes / 1e9, input_gen_s=t_gen,
+                           input_gen="host synth/ (PCG64)" if args.host_gen else
+                           "device gfq_simulate (Philox4x32-10, seed 0x%x)" % seed),
+               gathered_frames=len(res.frames))
+    if not full:
+        return out
 
     # ---------------- e2e through the host-buffer C-ABI entry
-    e2e = None
     if not args.no_e2e:
         s_host = torch.empty((F, cfg.N), dtype=torch.uint8).pin_memory()
         it_host = torch.empty(F, dtype=torch.int32).pin_memory()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(steps):
             for s in schedules:
                 gfq.gfq_decode_host(gcode, obs_host, params[s], s_host, it_host, ws, stream)
         t_e2e = time.perf_counter() - t0
         if world > 1:
             t_e2e = shard.max_over_ranks(t_e2e, dist, device="cuda")
-        e2e = dict(value=bits_per_step_rank * world * args.steps / t_e2e, unit="bit/s",
-                   h2d_bytes_per_step=int(obs_host.numel() * obs_host.element_size() * len(schedules)),
-                   d2h_bytes_per_step=int((s_host.numel() + it_host.numel() * 4) * len(schedules)))
+        out["e2e"] = dict(value=bits_per_step_rank * world * steps / t_e2e, unit="bit/s",
+                          h2d_bytes_per_step=int(obs_host.numel() * obs_host.element_size() * len(schedules)),
+                          d2h_bytes_per_step=int((s_host.numel() + it_host.numel() * 4) * len(schedules)))
 
-    # ---------------- convergence run (paper's SUS/PUS iteration ratio), untimed
-    conv = None
+    # ---------------- convergence run (paper's SUS/PUS iteration ratio), untimed;
+    # early-exit cost against the ideal (mean iterations x per-iteration time)
     if not args.no_convergence and rank == 0:
         nf = min(args.conv_frames, F)
         obs_c = obs[:nf].contiguous()
         its = {}
-        for s in schedules:
-            pc = gfq.Params(ch, fr.ch_param, s, cfg.max_iters, early_exit=True, markov_T=T)
-            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            c0.record(stream)
-            sh, ic, _ = gfq.gfq_decode(gcode, obs_c, pc, workspace=ws, stream=stream)
-            c1.record(stream)
-            torch.cuda.synchronize()
-            its[("ms", s)] = c0.elapsed_time(c1)
-            its[s] = ic.cpu().numpy()
-            errs = (sh.cpu().numpy() != truth[:nf]).any(axis=1)
-            its[("fer", s)] = float(errs.mean())
         conv = dict(frames=nf, max_iters=cfg.max_iters)
         for s in schedules:
             name = "pus" if s == gfq.GFQ_PUS else "sus"
+            pc = gfq.Params(ch, param, s, cfg.max_iters, early_exit=True, markov_T=T)
+            sh, ic, _ = gfq.gfq_decode(gcode, obs_c, pc, workspace=ws, stream=stream)   # warm-up
+            c_ms = timer(lambda: gfq.gfq_decode(gcode, obs_c, pc, sh, ic, ws, stream))
+            its[s] = ic.cpu().numpy()
+            errs = (sh.cpu().numpy() != truth[:nf]).any(axis=1)
+            # per-iteration time at this batch: a fixed 10-iteration decode of the same frames
+            pf = gfq.Params(ch, param, s, 10, early_exit=False, markov_T=T)
+            f_ms = timer(lambda: gfq.gfq_decode(gcode, obs_c, pf, sh, ic, ws, stream)) / 10.0
             ok = its[s] > 0
+            spent = np.where(ok, its[s], cfg.max_iters).astype(float)
             conv[name] = dict(mean_iters=float(its[s][ok].mean()) if ok.any() else None,
-                              nonconverged=int((~ok).sum()), frame_error_rate=its[("fer", s)],
-                              ms_to_converge=its[("ms", s)])
+                              nonconverged=int((~ok).sum()), frame_error_rate=float(errs.mean()),
+                              ms_to_converge=c_ms, ms_per_iteration_full_batch=f_ms,
+                              ideal_ms=float(spent.mean() * f_ms),
+                              measured_over_ideal=float(c_ms / (spent.mean() * f_ms)))
         if len(schedules) == 2:
             both = (its[schedules[0]] > 0) & (its[schedules[1]] > 0)
             if both.any():
                 tp, ts = its[schedules[0]][both].astype(float), its[schedules[1]][both].astype(float)
                 conv.update(paired=int(both.sum()), ratio_of_means=float(ts.mean() / tp.mean()),
                             mean_ratio=float((ts / tp).mean()), std_ratio=float((ts / tp).std()))
+        out["convergence"] = conv
 
-    # ---------------- CPU oracle baseline (rank 0, N=1 only)
-    cpu = None
+    # ---------------- CPU oracle baseline (rank 0, N=1 only): ~10-30 s of the box's cores
     if not args.no_cpu and rank == 0 and world == 1:
         ncores = os.cpu_count() or 1
-        si = 1 if cfg.q >= 64 else 2
-        sf = max(1, min(ncores, 32))
-        sample = argparse.Namespace(channel=fr.channel, ch_param=fr.ch_param, obs=obs_host[:sf].numpy())
+        si = 2
+        sf = max(1, min(2 * ncores, 64))
+        sample = argparse.Namespace(channel=cfg.channel, ch_param=param, obs=obs_host[:sf].numpy())
         dt, thr = oracle_sample_rate(cfg, code, sample, sf, si, [0 if s == gfq.GFQ_PUS else 1 for s in schedules])
         t_full = dt * iters / si
-        cpu = dict(value=len(schedules) * sf * cfg.N * cfg.p / t_full, unit="bit/s", cores=thr, kind="oracle",
-                   sample="%d frames x %d iteration(s) per schedule, extrapolated linearly to %d iterations"
-                          % (sf, si, iters), seconds=dt)
+        out["cpu_baseline"] = dict(value=len(schedules) * sf * cfg.N * cfg.p / t_full, unit="bit/s", cores=thr,
+                                   kind="oracle",
+                                   sample="%d frames x %d iterations per schedule (fixed), extrapolated linearly "
+                                          "to %d iterations" % (sf, si, iters), seconds=dt)
+    del ws
+    torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    args = parse()
+    cfg = synth.CONFIGS[args.config]
+    iters = args.iters or cfg.fixed_iters or cfg.max_iters
+    F = args.frames or cfg.frames
+    if args.impl == "reference":
+        return run_reference(args, cfg, iters, F)
+    rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        from paper_cs_0605069_b200 import shard
+        return shard.relaunch_under_torchrun(args.gpus, [os.path.abspath(__file__)] + sys.argv[1:])
+    if world != args.gpus:
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%d" % (args.gpus, world))
+
+    import torch
+    import torch.distributed as dist
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device -- the decoder runs only on the GPU (no CPU fallback)")
+    if torch.cuda.device_count() <= local:
+        raise SystemExit("bench.py: rank %d needs cuda:%d, only %d device(s)" % (rank, local, torch.cuda.device_count()))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_cs_0605069_b200 import gfq, shard
+
+    schedules = [gfq.GFQ_PUS if s == "pus" else gfq.GFQ_SUS for s in args.schedules.split(",")]
+    head = decode_run(args, cfg, F, iters, schedules, args.steps, args.warmup, gfq, shard, dist, rank, world, local)
+    sec = None
+    if args.secondary and args.secondary != cfg.name:
+        c2 = synth.CONFIGS[args.secondary]
+        sec = decode_run(args, c2, c2.frames, args.secondary_iters, schedules, args.secondary_steps,
+                         max(3, min(args.warmup, 3)), gfq, shard, dist, rank, world, local, full=False)
+        sec.update(metric="decoded info-bits/s", unit="bit/s", steps=args.secondary_steps)
 
     if rank == 0:
         line = dict(
-            metric="decoded info-bits/s", value=value, unit="bit/s", n_gpus=world, steps=args.steps,
-            warmup=args.warmup, ms_per_step=ms / args.steps, higher_is_better=True, scaling="weak",
-            vs_baseline=None, dtype="f32", data="synthetic",
-            config=dict(workload(cfg, F, iters), arith="fp64 registers, fp32 message storage",
-                        parallelism="frame-sharded dp%d (no collective)" % world,
-                        l2="inputs larger than L2 (message state %.1f GB/GPU vs 126 MB)" %
-                           (cfg.E * cfg.q * 4 * F * 2 / 1e9),
-                        workspace_gb=ws_bytes / 1e9, input_gen_s=t_gen,
-                        input_gen="host synth/ (PCG64)" if args.host_gen else
-                        "device gfq_simulate (Philox4x32-10, seed 0x%x)" % (0xBE7C0000 + cfg.cid * 64 + args.point)),
-            edge_msg_updates_per_s=edge_updates / (ms / 1e3),
-            model_hbm_gbs=model_gbs,
-            roofline=roof, cpu_baseline=cpu, e2e=e2e, clocks=clk,
-            gpu_launches=int(launches_timed),
-            kernels={k: dict(ms=v[0], launches=v[1]) for k, v in kinds.items()},
-            health=dict(zero_normalisers_last_decode=st["zero_normalisers"]),
-            convergence=conv,
+            metric="decoded info-bits/s", value=head["value"], unit="bit/s", n_gpus=world, steps=args.steps,
+            warmup=args.warmup, ms_per_step=head["ms_per_step"], higher_is_better=True, scaling="weak",
+            vs_baseline=None, dtype="f32 storage / f64 arithmetic", data="synthetic",
+            config=head["config"],
+            edge_msg_updates_per_s=head["edge_msg_updates_per_s"], model_hbm_gbs=head["model_hbm_gbs"],
+            ms_per_step_instrumented=head["ms_per_step_instrumented"],
+            roofline=head["roofline"], rooflines=head["rooflines"], cpu_baseline=head.get("cpu_baseline"),
+            e2e=head.get("e2e"), clocks=head["clocks"], gpu_launches=head["gpu_launches"],
+            kernels=head["kernels"], health=head["health"], convergence=head.get("convergence"),
+            secondary=sec,
         )
         print(json.dumps(line), flush=True)
     if world > 1:

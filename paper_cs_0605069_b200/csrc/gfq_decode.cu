@@ -13,6 +13,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <utility>
 #include <vector>
 
 #include "gfq_internal.cuh"
@@ -202,9 +205,15 @@ struct LagRing {
   }
 };
 
-static LagRing &lag_ring() {
-  static thread_local LagRing r;
-  return r;
+// One ring per (device, stream) of the calling thread: its events belong to
+// that device, and a D2H readback still queued from an earlier decode on the
+// same stream completes before this decode's own copies (stream order), so a
+// slot is never read while another decode's copy into it is pending.
+static LagRing &lag_ring(int dev, cudaStream_t st) {
+  static thread_local std::map<std::pair<int, cudaStream_t>, std::unique_ptr<LagRing>> rings;
+  std::unique_ptr<LagRing> &r = rings[std::make_pair(dev, st)];
+  if (!r) r.reset(new LagRing());
+  return *r;
 }
 
 // mode: 0 BSC, 1 BEC, 2 BI-AWGN (obs), 3 evidence (hard_in + pi_in)
@@ -221,6 +230,10 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
   int dev = -1;
   cudaError_t ce = cudaGetDevice(&dev);
   if (ce != cudaSuccess) return cuda_fail(ce, "cudaGetDevice");
+  if (dev != c->device) {
+    set_error("the current CUDA device is not the one the code was created on");
+    return GFQ_EINVAL;
+  }
   const int fbt = (F + 31) / 32;
   const int fbw = blocks_fitting(c, prm, ws_bytes, fbt);
   if (fbw < 1) { set_error("workspace too small for one 32-frame block"); return GFQ_EINVAL; }
@@ -279,7 +292,7 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
     if (ce != cudaSuccess) return cuda_fail(ce, "clear trace");
   }
 
-  LagRing &ring = lag_ring();
+  LagRing &ring = lag_ring(dev, st);
   unsigned long long launches = 0;
   int rc = GFQ_OK;
   Profiler &prof = profiler();
@@ -473,14 +486,18 @@ extern "C" int gfq_decode_host(const gfq_code *c, int n_frames, const void *obs_
     return GFQ_EINVAL;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  // the decode workspace starts at offset 0 (gfq_decode_stats and
+  // gfq_export_messages read it there); the staging copies sit at the end
   char *base = (char *)ws;
-  void *obs_d = base;
-  unsigned char *s_d = (unsigned char *)(base + ob);
-  int *it_d = (int *)(base + ob + sb);
+  const size_t dec_bytes = (ws_bytes - (ob + sb + ib)) & ~(size_t)255;
+  char *stg = base + dec_bytes;
+  void *obs_d = stg;
+  unsigned char *s_d = (unsigned char *)(stg + ob);
+  int *it_d = (int *)(stg + ob + sb);
   cudaError_t ce = cudaMemcpyAsync(obs_d, obs_host, obs_bytes(c, n_frames, prm), cudaMemcpyHostToDevice, st);
   if (ce != cudaSuccess) return cuda_fail(ce, "copy obs to device");
   rc = decode_common(c, n_frames, prm->channel, prm->ch_param, obs_d, nullptr, nullptr, prm, s_d, c->N,
-                     it_d, base + ob + sb + ib, ws_bytes - (ob + sb + ib), st);
+                     it_d, base, dec_bytes, st);
   if (rc) return rc;
   ce = cudaMemcpyAsync(s_hat_host, s_d, (size_t)n_frames * c->N, cudaMemcpyDeviceToHost, st);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(iters_host, it_d, sizeof(int) * n_frames, cudaMemcpyDeviceToHost, st);

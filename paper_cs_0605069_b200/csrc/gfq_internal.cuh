@@ -152,6 +152,8 @@ int launch_init_state(const WaveArgs &a, cudaStream_t s);
 int launch_cn(const WaveArgs &a, cudaStream_t s);
 int launch_vn(const WaveArgs &a, cudaStream_t s);
 int launch_sus_level(const WaveArgs &a, int level, int ncols, cudaStream_t s);
+bool sus_dc_applies(const WaveArgs &a);   // gfq_sus_dc.cu
+int launch_sus_dc(const WaveArgs &a, int level, int ncols, cudaStream_t s);
 int launch_test(const WaveArgs &a, cudaStream_t s);
 int launch_finalize(const WaveArgs &a, int final_pass, cudaStream_t s);
 int launch_capture(const WaveArgs &a, unsigned char *out, int L, int mode, cudaStream_t s);

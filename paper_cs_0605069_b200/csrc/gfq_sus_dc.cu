@@ -1,0 +1,388 @@
+// gfq_sus_dc.cu -- the SUS level kernel for small fields (q <= 16) by direct
+// convolution: PAPER.md §2, SUS steps 1-4 with the check-node
+// update Eq. (3) evaluated as the sum over configurations it is.
+//
+// Why a second SUS kernel.  In the transform formulation (gfq_bp.cu) a SUS
+// unit (one check of one column) forward-transforms the d-1 other messages of
+// the check, multiplies, and inverse-transforms; in fp64 (the inverse
+// transform produces small probabilities by cancellation) and, for q = 16,
+// with the q-vector split over two warps (layout switches through shared
+// memory, group barriers).  For q <= 16 the direct sum is as cheap: the XOR-
+// convolution S = u_1 (*) u_2 (*) ... of the permuted other messages costs
+// q^2 fused multiply-adds per factor, all terms are non-negative (no
+// cancellation: fp32 keeps every entry to a relative ~q ulps, including the
+// tiny ones), and a whole q-vector fits one thread's registers.  So one warp
+// owns a unit for its 32 frames (one frame per lane): no layout switches, no
+// cross-warp barriers, every warp an independent TMA pipeline.
+//
+//   u_k(y) = q_ij_k(h_k^-1 y)           (distribution of h_k x_k; rows chosen at load)
+//   S(y)   = sum_{x_1 ^ ... ^ x_{d-1} = y} prod_k u_k(x_k)   (fp32, FFMA2 pairs)
+//   r_ij(a) = S(z_i ^ h_ij a)           (Eq. 3: the check sum equals z_i, reading A4)
+// S is stored to the warp's shared r slots at row a = h^-1 y ^ h^-1 z (per-lane
+// z: a per-lane XOR of the row; rows are 128-byte lines of 32 lanes, so the
+// access is bank-conflict free).  The variable update of the column (Eq. 4,
+// posterior Eq. 5, clipping) is vn_core in fp64 registers, as in the other
+// kernels.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gfq_device.cuh"
+#include "gfq_launch.cuh"
+
+namespace gfq {
+
+// warps per CTA / stages per warp (tuning knobs)
+#ifndef GFQ_DC_W
+#define GFQ_DC_W 8
+#endif
+#ifndef GFQ_DC_S
+#define GFQ_DC_S 3
+#endif
+#ifndef GFQ_DC_S_MARKOV
+#define GFQ_DC_S_MARKOV 3
+#endif
+#ifndef GFQ_DC_FFMA2
+#define GFQ_DC_FFMA2 1
+#endif
+
+template <int Q, int DMAX, int DVMAX, bool MARKOV, int S, int W>
+struct DCShape {
+  // the stage's extra rows: the p per-bit flip probabilities of a noise
+  // column; a Markov source column's neighbour posteriors are read from L2
+  // (prefetched when its first unit is issued) instead of taking 2q rows of
+  // every stage
+  static constexpr int XR = Extra<Q, false>::rows;
+  static constexpr size_t PAY = (size_t)(DMAX - 1) * Q * 128;  // the d-1 other messages
+  static constexpr size_t RSM = (size_t)DVMAX * Q * 128;        // fp32 r of the column's checks
+  static constexpr size_t TSM_B = (MARKOV ? (size_t)2 * Q * Q * 4 : 0) + (size_t)2 * Q * Q;
+  using Sh = Shape<Q, S, W, PAY, RSM, (size_t)XR * 128, TSM_B, false>;
+  static constexpr size_t SMEM = Sh::SMEM;
+  static constexpr int THREADS = W * 32;
+};
+
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Rows of the Markov neighbours j-1 / j+1 that source column j reads (reading
+// A9 snapshot or A34 in-sweep, markov_nbrs), or null.
+template <int Q>
+__device__ __forceinline__ void markov_rows(const WaveArgs &a, int fb, int j, const float *&left,
+                                            const float *&right) {
+  const int N = a.c.N;
+  const int nb = markov_nbrs(a, j);
+  left = (nb & 1) ? (a.gs ? a.qs_new : a.qs_old) + ((size_t)fb * N + (j - 1)) * Q * 32 : nullptr;
+  right = (nb & 2) ? a.qs_old + ((size_t)fb * N + (j + 1)) * Q * 32 : nullptr;
+}
+
+// One SUS unit (column, check slot) into a stage: as sus_issue (gfq_device.cuh),
+// with only the noise rows as extras; a Markov source column's neighbour
+// posteriors are prefetched into L2 with its first unit.
+template <int Q, int DMAX, bool MARKOV>
+__device__ __forceinline__ bool dc_issue(const WaveArgs &a, int fb, int col, int &s, int lvl_begin,
+                                         unsigned char *hdr, unsigned char *pay, unsigned char *xtra,
+                                         uint64_t *full) {
+  const LvlCol lc = a.c.lvl_col[lvl_begin + col];
+  const int nunits = lc.dv > 0 ? lc.dv : 1;
+  const LvlUnit un = a.c.lvl_unit[lc.unit0 + s];
+  TaskInfo *ti = (TaskInfo *)hdr;
+  ti->fb = fb; ti->item = lc.j; ti->e0 = lc.e0; ti->deg = lc.dv;
+  ti->s = s; ti->r0 = un.r0; ti->d = un.d; ti->pos = un.pos; ti->i = un.i;
+  const bool last = (s == nunits - 1);
+  if (MARKOV && s == 0 && lc.j < a.c.N) {
+    const float *l, *r;
+    markov_rows<Q>(a, fb, lc.j, l, r);
+    if (l) prefetch_l2(l, Q * 128);
+    if (r) prefetch_l2(r, Q * 128);
+  }
+  uint32_t b0 = 0, b1 = 0;
+  const float *rowbase = a.qmsg + ((size_t)fb * a.c.E + un.r0) * Q * 32;
+  if (lc.dv > 0) {
+    b0 = (uint32_t)un.pos * Q * 128;
+    b1 = (uint32_t)(un.d - 1 - un.pos) * Q * 128;
+  }
+  const uint32_t bx = last ? 64 + extras_bytes<Q, false>(a, lc.j) : 0;
+  mbar_expect_tx(full, (lc.dv > 0 ? 64 + 32 : 0) + (a.early_exit ? 128 : 0) + b0 + b1 + bx);
+  if (lc.dv > 0) {
+    bulk_g2s(hdr + 128, a.c.sus_desc + lc.e0 + s, 64, full);
+    bulk_g2s(hdr + 256, a.z + ((size_t)fb * a.c.M + un.i) * 32, 32, full);
+  }
+  if (a.early_exit) bulk_g2s(hdr + 384, a.conv + fb * 32, 128, full);
+  if (b0) bulk_g2s(pay, rowbase, b0, full);
+  if (b1) bulk_g2s(pay + (size_t)un.pos * Q * 128, rowbase + (size_t)(un.pos + 1) * Q * 32, b1, full);
+  if (last) {
+    bulk_g2s(hdr + 192, a.c.var_desc + lc.j, 64, full);
+    issue_extras<Q, false>(a, fb, lc.j, xtra, full);
+  }
+  if (++s >= nunits) {
+    s = 0;
+    return true;
+  }
+  return false;
+}
+
+// u[y] = message(h^-1 y) for y = 0..Q-1 from a stage slot (fp32 rows of 32 lanes)
+template <int Q>
+__device__ __forceinline__ void dc_load(uint32_t slot_lane, uint32_t rt, unsigned long long pk, float (&u)[Q]) {
+  uint32_t ad[Q];
+  tab_addrs_sm<Q, Q>(slot_lane, rt, pk, 0, ad);
+#pragma unroll
+  for (int y = 0; y < Q; ++y) u[y] = lds_f32(ad[y]);
+}
+
+// s[y] = sum_x u[x] v[y ^ x]  (XOR convolution; x ascending)
+template <int Q>
+__device__ __forceinline__ void dc_conv(const float (&u)[Q], const float (&v)[Q], float (&s)[Q]) {
+#if GFQ_DC_FFMA2
+  if constexpr (Q >= 4) {
+    // pairs (s[2m], s[2m+1]) += u[x] * (v[2m ^ x], v[2m+1 ^ x]): for even x the
+    // pair of v is (v[2m^x], v[(2m^x)+1]) in order, for odd x it is swapped
+    unsigned long long vp[Q / 2], vs[Q / 2], acc[Q / 2];
+#pragma unroll
+    for (int m = 0; m < Q / 2; ++m) {
+      vp[m] = ((unsigned long long)__float_as_uint(v[2 * m + 1]) << 32) | __float_as_uint(v[2 * m]);
+      vs[m] = ((unsigned long long)__float_as_uint(v[2 * m]) << 32) | __float_as_uint(v[2 * m + 1]);
+    }
+#pragma unroll
+    for (int m = 0; m < Q / 2; ++m) {
+      const unsigned long long u0 = ((unsigned long long)__float_as_uint(u[0]) << 32) | __float_as_uint(u[0]);
+      asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(acc[m]) : "l"(u0), "l"(vp[m]));
+    }
+#pragma unroll
+    for (int x = 1; x < Q; ++x) {
+      const unsigned long long ux = ((unsigned long long)__float_as_uint(u[x]) << 32) | __float_as_uint(u[x]);
+#pragma unroll
+      for (int m = 0; m < Q / 2; ++m) {
+        const int src = m ^ (x >> 1);
+        const unsigned long long vv = (x & 1) ? vs[src] : vp[src];
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[m]) : "l"(ux), "l"(vv));
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < Q / 2; ++m) {
+      s[2 * m] = __uint_as_float((unsigned)(acc[m] & 0xffffffffu));
+      s[2 * m + 1] = __uint_as_float((unsigned)(acc[m] >> 32));
+    }
+    return;
+  }
+#endif
+#pragma unroll
+  for (int y = 0; y < Q; ++y) {
+    float acc = u[0] * v[y];
+#pragma unroll
+    for (int x = 1; x < Q; ++x) acc = fmaf(u[x], v[y ^ x], acc);
+    s[y] = acc;
+  }
+}
+
+// SUS step 1 for one check of the column (DO = d-1 other edges): S in fp32,
+// then q * r_ij (the scale of the transform kernels' stored r, which the
+// variable node normalises away) into r slot ti.s of the warp.
+template <int Q, int DO, typename RF>
+__device__ __forceinline__ void dc_check(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_lane, uint32_t rt,
+                                         float *rsm, int lane, bool frozen, bool release, uint64_t *empty,
+                                         RF &&refill) {
+  const TaskInfo ti = *(const TaskInfo *)hdr;
+  const SusDesc *sd = (const SusDesc *)(hdr + 128);
+  const int z = hdr[256 + lane];
+  const unsigned long long pke = sd->perm_e;
+  float S[Q];
+  if constexpr (DO == 0) {
+    // degree-1 check: the sum over no other variable is the point mass at 0
+    if (release) { release_stage(empty, lane); refill(); }
+#pragma unroll
+    for (int y = 0; y < Q; ++y) S[y] = (y == 0) ? 1.0f : 0.0f;
+  } else if constexpr (DO == 1) {
+    dc_load<Q>(pay_lane, rt, sd->perm_o[0], S);
+    if (release) { release_stage(empty, lane); refill(); }
+  } else {
+    float u[Q], v[Q];
+    dc_load<Q>(pay_lane, rt, sd->perm_o[0], u);
+    dc_load<Q>(pay_lane + Q * 128, rt, sd->perm_o[1], v);
+    if constexpr (DO == 2) {
+      if (release) { release_stage(empty, lane); refill(); }
+      dc_conv<Q>(u, v, S);
+    } else {
+      static_assert(DO == 3, "dc_check: check degree <= 4");
+      float w[Q], t[Q];
+      dc_load<Q>(pay_lane + 2 * Q * 128, rt, sd->perm_o[2], w);
+      if (release) { release_stage(empty, lane); refill(); }
+      dc_conv<Q>(u, v, t);
+      dc_conv<Q>(t, w, S);
+    }
+  }
+  // r(a) = S(z ^ h a): S[y] goes to row a = h^-1 y ^ h^-1 z
+  uint32_t ad[Q];
+  tab_addrs_sm<Q, Q>(0u, rt, pke, 0, ad);  // (h^-1 y) << 7
+  uint32_t hz;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(hz) : "r"(rt + (uint32_t)(((pke & 0xff) * Q + z) * 2)));
+  unsigned char *rs = (unsigned char *)(rsm + (size_t)ti.s * Q * 32 + lane);
+#pragma unroll
+  for (int y = 0; y < Q; ++y) *(float *)(rs + (ad[y] ^ hz)) = S[y] * (float)Q;
+  if (a.rmsg != nullptr && !frozen) {  // keep_messages only (export)
+    unsigned char *rd = (unsigned char *)(a.rmsg + ((size_t)ti.fb * a.c.E + ti.e0 + ti.s) * Q * 32 + lane);
+#pragma unroll
+    for (int y = 0; y < Q; ++y) *(float *)(rd + (ad[y] ^ hz)) = S[y] * (float)Q;
+  }
+}
+
+// SUS step 2 (+ step 4, reading A8) for the column: Eq. (4) for each of its
+// edges and the posterior Eq. (5) with clipping, from the fresh r's.
+template <int Q, int DV, bool MARKOV>
+__device__ __forceinline__ void dc_vn(const WaveArgs &a, const unsigned char *hdr, const unsigned char *xtra,
+                                      const float *Tsm, const float *rsm, int lane, bool frozen) {
+  const TaskInfo ti = *(const TaskInfo *)hdr;
+  const VarDesc *vd = (const VarDesc *)(hdr + 192);
+  int qdst[DV > 0 ? DV : 1];
+  double r[DV > 0 ? DV : 1][Q];
+#pragma unroll
+  for (int s = 0; s < DV; ++s) {
+    qdst[s] = vd->qdst[s];
+#pragma unroll
+    for (int k = 0; k < Q; ++k) r[s][k] = (double)rsm[((size_t)s * Q + k) * 32 + lane];
+  }
+  double pr[Q];
+  if (MARKOV && ti.item < a.c.N) {
+    const float *l, *r;
+    markov_rows<Q>(a, ti.fb, ti.item, l, r);   // L2-resident (prefetched with the first unit)
+    prior_from<Q, Q, MARKOV>(a, ti.item, 0, lane, l ? l : r, Tsm, pr, r ? r : l);
+  } else {
+    prior_from<Q, Q, MARKOV>(a, ti.item, 0, lane, (const float *)xtra, Tsm, pr);
+  }
+  vn_core<Q, Q, DV, MARKOV, false>(a, ti.fb, ti.item, qdst, r, pr, nullptr, 0, 0, lane, frozen);
+}
+
+template <int Q, int DMAX, int DVMAX, bool MARKOV, int S, int W>
+__global__ void __launch_bounds__(DCShape<Q, DMAX, DVMAX, MARKOV, S, W>::THREADS)
+    k_sus_dc(WaveArgs a, int lvl_begin, int ncols) {
+  using DS = DCShape<Q, DMAX, DVMAX, MARKOV, S, W>;
+  using Sh = typename DS::Sh;
+  static_assert(DMAX <= 4 && DVMAX <= 3, "k_sus_dc: check degree <= 4, variable degree <= 3");
+  extern __shared__ __align__(128) unsigned char smem[];
+  const SmemPtrs sp = smem_ptrs<Sh, S, W>(smem);
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  // programmatic dependent launch: the next level's CTAs may start their
+  // prologue now; everything after griddepcontrol.wait reads this level's output
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (threadIdx.x == 0) init_bars<S, W>(sp.bars, 1);
+  float *Tsm = sp.tsm;
+  if constexpr (MARKOV) {
+    if (a.Tf)
+      for (int k = threadIdx.x; k < 2 * Q * Q; k += blockDim.x) Tsm[k] = a.Tf[k];
+  }
+  unsigned short *rtab = (unsigned short *)(sp.tsm + (MARKOV ? 2 * Q * Q : 0));
+  for (int k = threadIdx.x; k < Q * Q; k += blockDim.x) rtab[k] = a.c.rowtab[k];
+  const uint32_t rt = smem_u32(rtab);
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const long long ntask = (long long)(*a.nactive) * ncols;
+  float *rsm = (float *)(sp.scr + (size_t)g * DS::RSM);
+  const bool producer = (lane == 0);
+  long long lo, hi;
+  group_range(ntask, (long long)blockIdx.x * W + g, (long long)gridDim.x * W, lo, hi);
+  Cursor pc;
+  int pu = 0;
+  if (producer) pc.init(a, lo, hi, ncols);
+  auto issue_next = [&](int k) {
+    if (!pc.valid()) return;
+    if (dc_issue<Q, DMAX, MARKOV>(a, pc.fb, pc.item, pu, lvl_begin, sp.hdr + (size_t)k * kHdr,
+                                   sp.pay + (size_t)k * Sh::PAYA, sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k))
+      pc.advance(a);
+  };
+  if (producer)
+    for (int n = 0; n < S; ++n) issue_next(g * S + n);
+  int rr = 0;  // units consumed by this warp
+  for (long long task = lo; task < hi; ++task) {
+    int nunits = 1;
+#pragma unroll 1
+    for (int s = 0; s < nunits; ++s, ++rr) {
+      const int st = rr % S, k = g * S + st;
+      const unsigned char *hdr = sp.hdr + (size_t)k * kHdr;
+      const unsigned char *xtra = sp.xtra + (size_t)k * Sh::XTRA_A;
+      const uint32_t pay_lane = sp.pay_u32 + (uint32_t)((size_t)k * Sh::PAYA) + lane * 4;
+      uint64_t *empty = sp.bars + W * S + k;
+      const int par = (rr / S) & 1;
+      auto refill = [&]() {
+        if (producer && pc.valid()) {
+          mbar_wait(empty, (uint32_t)par);
+          issue_next(k);
+        }
+      };
+      mbar_wait(sp.bars + k, (uint32_t)par);
+      const TaskInfo *ti = (const TaskInfo *)hdr;
+      const int dv = ti->deg, d = ti->d;
+      nunits = dv > 0 ? dv : 1;
+      const bool last = (s == nunits - 1);
+      const bool frozen = a.early_exit && ((const int *)(hdr + 384))[lane] != 0;
+      if (dv > 0) {
+        // the last unit's stage also carries the column's VarDesc and prior
+        // rows: it is released after the variable update
+        switch (d - 1) {
+          case 0: dc_check<Q, 0>(a, hdr, pay_lane, rt, rsm, lane, frozen, !last, empty, refill); break;
+          case 1: dc_check<Q, 1>(a, hdr, pay_lane, rt, rsm, lane, frozen, !last, empty, refill); break;
+          case 2: dc_check<Q, 2>(a, hdr, pay_lane, rt, rsm, lane, frozen, !last, empty, refill); break;
+          default: dc_check<Q, 3>(a, hdr, pay_lane, rt, rsm, lane, frozen, !last, empty, refill); break;
+        }
+      }
+      if (last) {
+        __syncwarp();  // the column's r slots are complete
+        switch (dv) {
+          case 0: dc_vn<Q, 0, MARKOV>(a, hdr, xtra, Tsm, rsm, lane, frozen); break;
+          case 1: dc_vn<Q, 1, MARKOV>(a, hdr, xtra, Tsm, rsm, lane, frozen); break;
+          case 2: dc_vn<Q, 2, MARKOV>(a, hdr, xtra, Tsm, rsm, lane, frozen); break;
+          default: dc_vn<Q, 3, MARKOV>(a, hdr, xtra, Tsm, rsm, lane, frozen); break;
+        }
+        release_stage(empty, lane);  // syncwarp: every lane is done with the r slots too
+        refill();
+      }
+    }
+  }
+}
+
+// most warps per CTA (<= want) whose stages fit the 227 KB of shared memory
+template <int Q, bool MK, int S>
+constexpr int dc_warps(int want) {
+  return (want <= 1 || DCShape<Q, 4, 3, MK, S, 1>::SMEM +
+                               (size_t)(want - 1) * (DCShape<Q, 4, 3, MK, S, 2>::SMEM - DCShape<Q, 4, 3, MK, S, 1>::SMEM) <=
+                           232448)
+             ? want
+             : dc_warps<Q, MK, S>(want - 1);
+}
+
+template <int Q, bool MK>
+static int dc_launch(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
+  constexpr int S = MK ? GFQ_DC_S_MARKOV : GFQ_DC_S, W = dc_warps<Q, MK, S>(GFQ_DC_W);
+  using DS = DCShape<Q, 4, 3, MK, S, W>;
+  static_assert(DS::SMEM <= 232448, "k_sus_dc: shared memory");
+  auto k = k_sus_dc<Q, 4, 3, MK, S, W>;
+  const int grid = grid_for(k, DS::THREADS, DS::SMEM, ((long long)a.nfb * ncols + W - 1) / W);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(DS::THREADS);
+  cfg.dynamicSmemBytes = DS::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k, a, lb, ncols);
+  if (e != cudaSuccess) return cuda_fail(e, "k_sus_dc");
+  return check_launch("k_sus_dc");
+}
+
+// Fields handled here: q = 16 (check degree <= 4, variable degree <= 3).
+bool sus_dc_applies(const WaveArgs &a) {
+  return a.c.q == 16 && a.c.max_cdeg <= 4 && a.c.max_vdeg <= 3;
+}
+
+int launch_sus_dc(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
+  switch (a.c.q) {
+    case 16: return a.markov ? dc_launch<16, true>(a, lb, ncols, s) : dc_launch<16, false>(a, lb, ncols, s);
+    default: break;
+  }
+  set_error("k_sus_dc: unsupported q");
+  return GFQ_EUNSUPPORTED;
+}
+
+}  // namespace gfq

@@ -118,6 +118,30 @@ def _dptr(t) -> int:
     return t.data_ptr()
 
 
+def _expect(t, name, dtype, shape, device=None, cuda=True):
+    """Marshalling checks: the C side trusts pointers and sizes completely."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("%s: expected a torch tensor" % name)
+    if t.dtype != dtype:
+        raise TypeError("%s: expected dtype %s, got %s" % (name, dtype, t.dtype))
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError("%s: expected shape %s, got %s" % (name, tuple(shape), tuple(t.shape)))
+    if not t.is_contiguous():
+        raise ValueError("%s: expected a contiguous tensor" % name)
+    if cuda and not t.is_cuda:
+        raise ValueError("%s: expected a CUDA tensor" % name)
+    if not cuda and t.is_cuda:
+        raise ValueError("%s: expected a host tensor" % name)
+    if device is not None and t.device != device:
+        raise ValueError("%s: on %s, expected %s" % (name, t.device, device))
+
+
+def _obs_dtype(params: "Params"):
+    import torch
+    return torch.float32 if params.c.channel == GFQ_BIAWGN else torch.uint8
+
+
 class Params:
     """gfq_params plus the host arrays it points to (kept alive)."""
 
@@ -190,12 +214,16 @@ def gfq_decode(code: Code, obs, params: Params, s_hat=None, iters=None, workspac
     """obs: CUDA tensor [F][M*p] (uint8 for BSC/BEC, float32 for BI-AWGN)."""
     import torch
     F = obs.shape[0]
+    _expect(obs, "obs", _obs_dtype(params), (F, code.M * code.p))
     if s_hat is None:
         s_hat = torch.empty((F, code.N), dtype=torch.uint8, device=obs.device)
     if iters is None:
         iters = torch.empty(F, dtype=torch.int32, device=obs.device)
     if workspace is None:
         workspace = alloc_workspace(gfq_workspace_bytes(code, F, params), obs.device)
+    _expect(s_hat, "s_hat", torch.uint8, (F, code.N), obs.device)
+    _expect(iters, "iters", torch.int32, (F,), obs.device)
+    _expect(workspace, "workspace", torch.uint8, (workspace.numel(),), obs.device)
     _check(lib().gfq_decode(code.h, F, _dptr(obs), params.ref(), _dptr(s_hat), _dptr(iters),
                             _dptr(workspace), workspace.numel(), _stream_ptr(stream)))
     return s_hat, iters, workspace
@@ -205,12 +233,18 @@ def gfq_decode_evidence(code: Code, hard_bits, bit_flip_prob, params: Params, x_
                         workspace=None, stream=None):
     import torch
     F = hard_bits.shape[0]
+    dev = hard_bits.device
+    _expect(hard_bits, "hard_bits", torch.uint8, (F, code.M * code.p))
+    _expect(bit_flip_prob, "bit_flip_prob", torch.float32, (F, code.M * code.p), dev)
     if x_hat is None:
-        x_hat = torch.empty((F, code.V), dtype=torch.uint8, device=hard_bits.device)
+        x_hat = torch.empty((F, code.V), dtype=torch.uint8, device=dev)
     if iters is None:
-        iters = torch.empty(F, dtype=torch.int32, device=hard_bits.device)
+        iters = torch.empty(F, dtype=torch.int32, device=dev)
     if workspace is None:
-        workspace = alloc_workspace(gfq_workspace_bytes(code, F, params), hard_bits.device)
+        workspace = alloc_workspace(gfq_workspace_bytes(code, F, params), dev)
+    _expect(x_hat, "x_hat", torch.uint8, (F, code.V), dev)
+    _expect(iters, "iters", torch.int32, (F,), dev)
+    _expect(workspace, "workspace", torch.uint8, (workspace.numel(),), dev)
     _check(lib().gfq_decode_evidence(code.h, F, _dptr(hard_bits), _dptr(bit_flip_prob), params.ref(),
                                      _dptr(x_hat), _dptr(iters), _dptr(workspace), workspace.numel(),
                                      _stream_ptr(stream)))
@@ -230,6 +264,10 @@ def gfq_decode_host(code: Code, obs_host, params: Params, s_hat_host=None, iters
     if workspace is None:
         workspace = alloc_workspace(gfq_workspace_bytes_host(code, F, params))
     obs_t = obs_t.contiguous()
+    _expect(obs_t, "obs_host", _obs_dtype(params), (F, code.M * code.p), cuda=False)
+    _expect(s_hat_host, "s_hat_host", torch.uint8, (F, code.N), cuda=False)
+    _expect(iters_host, "iters_host", torch.int32, (F,), cuda=False)
+    _expect(workspace, "workspace", torch.uint8, (workspace.numel(),))
     _check(lib().gfq_decode_host(code.h, F, obs_t.data_ptr(), params.ref(), s_hat_host.data_ptr(),
                                  iters_host.data_ptr(), _dptr(workspace), workspace.numel(),
                                  _stream_ptr(stream)))
@@ -240,6 +278,7 @@ def gfq_export_messages(code: Code, n_frames: int, workspace, params: Params, q=
                         stream=None):
     import torch
     dev = workspace.device
+    _expect(workspace, "workspace", torch.uint8, (workspace.numel(),))
     qo = torch.empty((n_frames, code.E, code.q), dtype=torch.float32, device=dev) if q else None
     ro = torch.empty((n_frames, code.E, code.q), dtype=torch.float32, device=dev) if r else None
     Qo = torch.empty((n_frames, code.V, code.q), dtype=torch.float32, device=dev) if Q else None

@@ -20,6 +20,12 @@ for sname in scheds:
     prm = gfq.Params(ch, fr.ch_param, sch, iters, early_exit=False, markov_T=T)
     s, it, ws = gfq.gfq_decode(gc, obs, prm)   # warm-up
     torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record()
+    gfq.gfq_decode(gc, obs, prm, s, it, ws)     # clean: no per-launch events
+    c1.record()
+    torch.cuda.synchronize()
+    clean = c0.elapsed_time(c1)
     gfq.gfq_profile_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -32,7 +38,8 @@ for sname in scheds:
     per_iter_bytes = 16.0 * cfg.E * cfg.q * nf   # model bytes per iteration (8q per edge-message update, 2E updates)
     k = {kk: round(v[0] / max(v[1], 1), 4) for kk, v in prof.items() if v[1] > 0}
     main = prof["cn"][0] + prof["vn"][0] if sch == gfq.GFQ_PUS else prof["sus"][0]
-    out[sname] = dict(total_ms=round(tot, 2), ms_per_iter=round(main / iters, 3),
+    out[sname] = dict(total_ms=round(tot, 2), clean_total_ms=round(clean, 2),
+                      clean_model_GBps=round(per_iter_bytes * iters / (clean / 1e3) / 1e9, 1), ms_per_iter=round(main / iters, 3),
                       model_GBps=round(per_iter_bytes * iters / (main / 1e3) / 1e9, 1),
                       per_launch_ms=k, zero_norm=gfq.gfq_decode_stats(gc, ws)["zero_normalisers"])
 print(json.dumps(out))

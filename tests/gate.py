@@ -57,3 +57,37 @@ def record(case: str, F: int, match, strict, n_allow, extra: str = "") -> int:
 
 def allowed(F: int) -> int:
     return int(np.floor(0.001 * F))
+
+
+def near_tie_symbols(Q, allow: float = TIE_ALLOW) -> int:
+    """Number of symbols (rows of Q [n][q]) whose posterior has a second value within
+    `allow` (relative) of its maximum: the symbols whose clipping fp32 may decide
+    differently from the fp64 oracle's strict argmax."""
+    Q = np.asarray(Q)
+    mx = Q.max(-1, keepdims=True)
+    return int(((Q >= mx * (1.0 - allow)).sum(-1) > 1).sum())
+
+
+def trace_gate(tg, tref, gpu_it, ref_it, p: int, oracle_Q_at):
+    """Fig. 1 trace comparison (correct source bits of x_hat^(t), t = 0..T).  A frame
+    matches if the traces are equal, or if both stop at the same iteration and at
+    every t where they differ |delta| <= p * (near-tie source symbols of the
+    oracle's posterior at t); oracle_Q_at(f, t) -> source posteriors [N][q] after t
+    iterations.  Returns (match [F] bool, n_allowance)."""
+    tg, tref = np.asarray(tg), np.asarray(tref)
+    match = (tg == tref).all(axis=1)
+    n_allow = 0
+    for f in np.where(~match)[0]:
+        if gpu_it[f] != ref_it[f]:
+            continue
+        ok = True
+        for t in np.where(tg[f] != tref[f])[0]:
+            t_eff = t if ref_it[f] < 0 else min(int(t), int(ref_it[f]))
+            amb = near_tie_symbols(oracle_Q_at(int(f), t_eff))
+            if abs(int(tg[f, t]) - int(tref[f, t])) > p * amb:
+                ok = False
+                break
+        if ok:
+            match[f] = True
+            n_allow += 1
+    return match, n_allow

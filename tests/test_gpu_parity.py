@@ -206,6 +206,44 @@ def test_host_entry_matches_device(gfq):
     assert torch.equal(sd.cpu(), sh) and torch.equal(itd.cpu(), ith)
 
 
+def test_host_entry_keeps_stats_and_export_at_offset_0(gfq):
+    """gfq_decode_host stages obs / results at the END of the workspace, so the
+    decode's health counters and messages stay where gfq_decode_stats and
+    gfq_export_messages read them."""
+    cfg, code, fr = _setup("C1", 40)
+    gcode = gfq.Code.from_synth(code)
+    prm = gfq.Params(gfq.GFQ_BSC, fr.ch_param, 1, 5, early_exit=False, keep_messages=True)
+    ws = gfq.alloc_workspace(gfq.gfq_workspace_bytes_host(gcode, fr.F, prm))
+    gfq.gfq_decode_host(gcode, torch.as_tensor(fr.obs).pin_memory(), prm, workspace=ws)
+    st = gfq.gfq_decode_stats(gcode, ws)
+    assert st["zero_normalisers"] == 0 and st["launches"] > 5 and st["block_iterations"] > 0
+    qh, rh, Qh = gfq.gfq_export_messages(gcode, fr.F, ws, prm)
+    _, _, _, wd = _gpu_decode(gfq, gcode, fr, 1, 5, False, keep=True)
+    qd, rd, Qd = gfq.gfq_export_messages(gcode, fr.F, wd, prm)
+    assert torch.equal(qh, qd) and torch.equal(rh, rd) and torch.equal(Qh, Qd)
+
+
+def test_marshalling_rejects_bad_buffers(gfq):
+    """The binding checks dtype, shape and device before calling the C ABI (which
+    trusts pointers and sizes): ADVICE r1."""
+    cfg, code, fr = _setup("C3", 4, 2)
+    gcode = gfq.Code.from_synth(code)
+    prm = gfq.Params(gfq.GFQ_BIAWGN, fr.ch_param, 0, 5)
+    obs = torch.as_tensor(fr.obs).cuda()
+    with pytest.raises(TypeError):
+        gfq.gfq_decode(gcode, obs.to(torch.uint8), prm)               # AWGN needs float32
+    with pytest.raises(ValueError):
+        gfq.gfq_decode(gcode, obs[:, :-1].contiguous(), prm)         # row length != M*p
+    with pytest.raises(ValueError):
+        gfq.gfq_decode(gcode, obs.cpu(), prm)                         # host buffer to the device entry
+    with pytest.raises(ValueError):
+        gfq.gfq_decode(gcode, obs, prm, s_hat=torch.empty((4, code.N - 1), dtype=torch.uint8, device="cuda"))
+    with pytest.raises(TypeError):
+        gfq.gfq_decode(gcode, obs, prm, iters=torch.empty(4, dtype=torch.int64, device="cuda"))
+    with pytest.raises(ValueError):
+        gfq.gfq_decode_host(gcode, fr.obs, prm, s_hat_host=torch.empty((4, code.N), dtype=torch.uint8).cuda())
+
+
 def test_natural_chain_labelling_many_levels(gfq):
     """B chain in natural order: the SUS dependency depth is ~M (serial); still exact."""
     cfg = synth.CONFIGS["C2"]
@@ -319,10 +357,17 @@ def test_trace_fig1(gfq, name, nframes, point, fixed, schedule):
     hard, pi = oracle.frontend(fr.channel, fr.ch_param, fr.obs)
     ref = oc.decode(hard, pi, schedule=schedule, max_iters=tmax, fixed=fixed, T=T, s_true=fr.s)
     tg = trace.cpu().numpy()
-    same = (tg == ref["trace"]).all(axis=1)
-    print(name, "trace mismatching frames", int((~same).sum()), "of", fr.F)
+
+    def q_at(f, t):
+        o = oc.decode(hard[f:f + 1], pi[f:f + 1], schedule=schedule, max_iters=t, fixed=fixed, T=T,
+                      keep_messages=True)
+        return o["Q"][0, :code.N]
+    same, n_allow = gate.trace_gate(tg, ref["trace"], iters.cpu().numpy(), ref["iters"], code.p, q_at)
+    gate.GATE_LOG.append("trace %-28s frames %5d  mismatch %3d  tie-allowance %3d" % (
+        "%s p%d %s %s" % (name, point, "SUS" if schedule else "PUS", "fixed" if fixed else "early-exit"),
+        fr.F, int((~same).sum()), n_allow))
     assert (tg >= 0).all() and (tg <= code.N * code.p).all()
-    assert int((~same).sum()) <= int(np.floor(0.001 * fr.F))
+    assert int((~same).sum()) <= gate.allowed(fr.F)
     # the count of the final estimate is the count of the returned s_hat
     sh = s_hat.cpu().numpy()
     bits = lambda a: np.unpackbits(a[..., None], axis=-1, bitorder="little")[..., :code.p]
@@ -370,7 +415,7 @@ def _low_degree_code(p, N, M, seed):
     return rows, cols, vals, A, B
 
 
-@pytest.mark.parametrize("p,markov", [(5, False), (6, False), (6, True)])
+@pytest.mark.parametrize("p,markov", [(4, False), (4, True), (5, False), (6, False), (6, True)])
 def test_low_degree_code_large_field_message_parity(gfq, p, markov):
     N, M = 30, 50
     for seed in range(300, 400):

@@ -1,7 +1,10 @@
-"""The N>1 path's host logic on CPU: world_size-2 gloo processes shard the frames
-with no overlap, decode their shards independently (oracle stands in for the GPU
-here), and the gathered result equals the single-process decode; timings reduce
-with MAX."""
+"""The N>1 path's host logic on CPU: world_size-2 gloo processes run bench.py's
+per-rank entry (paper_cs_0605069_b200.shard.run_rank: frame range, warm-up,
+barrier, timed steps, max over ranks, gather) with only the decode call stubbed
+(the fp64 oracle stands in for libgfq on a CPU box); the shards are disjoint
+and complete, the gathered per-frame iteration counts equal a single-process
+decode, and the job time is the slowest rank's."""
+import time
 import os
 import socket
 
@@ -40,13 +43,27 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        ids = shard.frame_range(rank, world, F_PER_RANK)
-        x, it = _decode(list(ids))
-        got = shard.gather_objects((list(ids), x, it), dist)
-        tmax = shard.max_over_ranks(float(rank + 1), dist)
+        state = {}
+        calls = []
+
+        def step(ids):                     # the stubbed decode call
+            calls.append(list(ids))
+            x, it = _decode(list(ids))
+            state["x"], state["it"] = x, it
+            if rank == 1:
+                time.sleep(0.2)            # rank 1 is the slow one
+
+        def timer(fn):                     # bench.py: CUDA events on the stream
+            t0 = time.perf_counter()
+            fn()
+            return (time.perf_counter() - t0) * 1e3
+
+        res = shard.run_rank(step, F_PER_RANK, steps=2, warmup=1, timer=timer, dist=dist,
+                             last_iters=lambda: [int(v) for v in state["it"]])
+        xs = shard.gather_objects(state["x"], dist)
         tsum = shard.sum_over_ranks(1.0, dist)
         if rank == 0:
-            q.put((got, tmax, tsum))
+            q.put((res.frames, res.iters, res.ms, res.ms_max, calls, xs, tsum))
     finally:
         dist.destroy_process_group()
 
@@ -62,14 +79,14 @@ def test_two_rank_gloo_sharding_matches_single_process():
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
-    got, tmax, tsum = q.get()
-    ids = [i for part in got for i in part[0]]
-    assert ids == list(range(world * F_PER_RANK))            # disjoint, complete, in rank order
-    x_all = np.concatenate([part[1] for part in got])
-    it_all = np.concatenate([part[2] for part in got])
-    x_ref, it_ref = _decode(ids)
-    assert np.array_equal(x_all, x_ref) and np.array_equal(it_all, it_ref)
-    assert tmax == 2.0 and tsum == 2.0
+    frames, iters, ms0, ms_max, calls, xs, tsum = q.get()
+    assert frames == list(range(world * F_PER_RANK))          # disjoint, complete, in rank order
+    assert calls == [list(range(F_PER_RANK))] * 3              # rank 0: 1 warm-up + 2 timed steps
+    x_ref, it_ref = _decode(frames)
+    assert np.array_equal(np.asarray(iters), it_ref)
+    assert np.array_equal(np.concatenate(xs), x_ref)
+    assert ms_max >= 400.0 and ms_max >= ms0                   # the slow rank sets the job time
+    assert tsum == 2.0
 
 
 def test_frame_range_validation():
