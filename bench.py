@@ -217,7 +217,10 @@ def decode_run(args, cfg, F, iters, schedules, steps, warmup, gfq, shard, dist, 
     """One workload: inputs on the device, `warmup` + `steps` clean timed steps through
     shard.run_rank, one instrumented step for the per-kernel times, the roofline of
     every hot kernel; with full=True also e2e, convergence and the CPU baseline."""
+    import gc
     import torch
+    gc.collect()
+    torch.cuda.empty_cache()          # a previous workload's cached blocks back to the driver
     code = synth.code_for(cfg)
     gcode = gfq.Code.from_synth(code)
     T = synth.markov_T_for(cfg)

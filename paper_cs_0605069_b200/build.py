@@ -57,6 +57,41 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
     return lib
 
 
+SYNC_CHECK_LIB = os.path.join(HERE, "libgfq_synccheck.so")
+KERNEL_SOURCES = ("gfq_bp.cu", "gfq_sus_dc.cu")   # the ones GFQ_SYNC_CHECK changes
+
+
+def build_sync_check(force: bool = False) -> str:
+    """libgfq_synccheck.so: the hot kernels with a full group barrier at every
+    elided one (GFQ_SYNC_CHECK=1, gfq_device.cuh), linked with the default
+    objects of the other sources.  tests/test_gpu_sync_check.py requires its
+    outputs to be bit-identical to libgfq.so's."""
+    build()
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh"))]
+    deps.append(os.path.join(HERE, "..", "include", "gfq.h"))
+    if (not force and os.path.exists(SYNC_CHECK_LIB)
+            and os.path.getmtime(SYNC_CHECK_LIB) > max(os.path.getmtime(d) for d in deps)):
+        return SYNC_CHECK_LIB
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(src):
+        obj = os.path.join(CSRC, src.replace(".cu", "_synccheck.o"))
+        cmd = [NVCC, *FLAGS, "-DGFQ_SYNC_CHECK=1", "-c", os.path.join(CSRC, src), "-o", obj]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError("nvcc failed for %s (sync check):\n%s" % (src, res.stderr[-8000:]))
+        return obj
+    with ThreadPoolExecutor(max_workers=len(KERNEL_SOURCES)) as ex:
+        objs = list(ex.map(one, KERNEL_SOURCES))
+    objs += [os.path.join(CSRC, f.replace(".cu", ".o")) for f in SOURCES if f not in KERNEL_SOURCES]
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", SYNC_CHECK_LIB, *objs,
+           "-Xcompiler", "-fPIC"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("link failed:\n%s" % res.stderr[-8000:])
+    return SYNC_CHECK_LIB
+
+
 if __name__ == "__main__":
     import sys
     defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]

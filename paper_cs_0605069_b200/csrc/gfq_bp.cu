@@ -72,6 +72,7 @@ __device__ __forceinline__ void xpose(double (&u)[D][KR], double *buf, int &m, i
     for (int s = 0; s < D; ++s) {
       double *b = buf + (size_t)(m & 1) * Q * 32;
       ++m;
+      elided_bar<T>(g);  // ping-pong: the buffer is rewritten without a barrier
 #pragma unroll
       for (int k = 0; k < KR; ++k) b[(A2B ? idxA<Q, KR>(c, k) : idxB<Q, KR>(c, k)) * 32 + lane] = u[s][k];
       group_bar<T>(g);
@@ -95,6 +96,7 @@ __device__ __forceinline__ void xpose_pairs(double (&u)[D][KR], double *X0, doub
   for (int p0 = 0; p0 < D; p0 += 2) {
     double *b = (t & 1) ? X1 : X0;
     ++t;
+    elided_bar<T>(g);  // pairs alternate between two buffers without a barrier
 #pragma unroll
     for (int s = p0; s < p0 + 2 && s < D; ++s)
 #pragma unroll
@@ -136,9 +138,13 @@ struct CNShape {
 
 template <int Q, int DMAX>
 __device__ __forceinline__ void cn_issue(const WaveArgs &a, int fb, int i, unsigned char *hdr, unsigned char *pay,
-                                         uint64_t *full) {
+                                         uint64_t *full, int e0 = -1, int e1 = -1) {
   const int M = a.c.M;
-  const int e0 = __ldg(a.c.row_ptr + i), d = __ldg(a.c.row_ptr + i + 1) - e0;
+  if (e0 < 0) {  // not prefetched (generic producer)
+    e0 = __ldg(a.c.row_ptr + i);
+    e1 = __ldg(a.c.row_ptr + i + 1);
+  }
+  const int d = e1 - e0;
   TaskInfo *ti = (TaskInfo *)hdr;
   ti->fb = fb; ti->item = i; ti->e0 = e0; ti->deg = d;
   const uint32_t msg = (uint32_t)d * Q * 128;
@@ -265,9 +271,12 @@ __global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(Wave
   Cursor pc;
   if (producer) {
     pc.init(a, lo, hi, M);
-    for (int n = 0; n < S && pc.valid(); ++n, pc.advance(a)) {
+    pc.load_range(a.c.row_ptr);
+    for (int n = 0; n < S && pc.valid(); ++n) {
       const int k = g * S + n;
       cn_issue<Q, DMAX>(a, pc.fb, pc.item, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA, sp.bars + k);
+      pc.advance(a);
+      pc.load_range(a.c.row_ptr);
     }
   }
   for (long long task = lo; task < hi; ++task) {
@@ -282,6 +291,7 @@ __global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(Wave
         mbar_wait(empty, (uint32_t)((rr / S) & 1));
         cn_issue<Q, DMAX>(a, pc.fb, pc.item, hdrw, sp.pay + (size_t)k * Sh::PAYA, sp.bars + k);
         pc.advance(a);
+        pc.load_range(a.c.row_ptr);
       }
     };
     mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
@@ -305,6 +315,7 @@ __global__ void __launch_bounds__(CNShape<Q, KR, DMAX, S, G>::THREADS) k_cn(Wave
         }
         break;
     }
+    elided_bar<T>(g);  // tasks follow each other without a barrier
   }
 }
 
@@ -327,9 +338,13 @@ struct VNShape {
 
 template <int Q, int DVMAX, bool MARKOV>
 __device__ __forceinline__ void vn_issue(const WaveArgs &a, int fb, int j, unsigned char *hdr, unsigned char *pay,
-                                         unsigned char *xtra, uint64_t *full, int clip_only) {
-  const int e0 = __ldg(a.c.col_ptr + j);
-  const int dv = clip_only ? 0 : __ldg(a.c.col_ptr + j + 1) - e0;
+                                         unsigned char *xtra, uint64_t *full, int clip_only, int e0 = -1,
+                                         int e1 = -1) {
+  if (e0 < 0) {  // not prefetched (generic producer)
+    e0 = __ldg(a.c.col_ptr + j);
+    e1 = __ldg(a.c.col_ptr + j + 1);
+  }
+  const int dv = clip_only ? 0 : e1 - e0;
   TaskInfo *ti = (TaskInfo *)hdr;
   ti->fb = fb; ti->item = j; ti->e0 = e0; ti->deg = dv;
   const uint32_t br = (uint32_t)dv * Q * 128;
@@ -401,10 +416,13 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
   Cursor pc;
   if (producer) {
     pc.init(a, lo, hi, V);
-    for (int n = 0; n < S && pc.valid(); ++n, pc.advance(a)) {
+    pc.load_range(a.c.col_ptr);
+    for (int n = 0; n < S && pc.valid(); ++n) {
       const int k = g * S + n;
       vn_issue<Q, DVMAX, MARKOV>(a, pc.fb, pc.item, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA,
                                  sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k, clip_only);
+      pc.advance(a);
+      pc.load_range(a.c.col_ptr);
     }
   }
   for (long long task = lo; task < hi; ++task) {
@@ -420,6 +438,7 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
         vn_issue<Q, DVMAX, MARKOV>(a, pc.fb, pc.item, hdrw, sp.pay + (size_t)k * Sh::PAYA,
                                    sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k, clip_only);
         pc.advance(a);
+        pc.load_range(a.c.col_ptr);
       }
     };
     mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
@@ -447,6 +466,7 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
     }
 #undef VT
     // no barrier here: vn_core's own barriers order every reuse of red
+    elided_bar<T>(g);
   }
 }
 
@@ -612,6 +632,7 @@ __device__ __forceinline__ void sus_check_phased(const WaveArgs &a, const unsign
 #pragma unroll
     for (int t = 0; t < DO; ++t) wht_bits<KR, 0, LKR>(v[t]);
     constexpr int D1 = DO < 2 ? DO : 2;
+    elided_bar<T>(g);  // xp reused across units without a barrier
 #pragma unroll
     for (int t = 0; t < D1; ++t)
 #pragma unroll
@@ -642,6 +663,7 @@ __device__ __forceinline__ void sus_check_phased(const WaveArgs &a, const unsign
       acc[k] = flip(x, sm[k]);
     }
     wht_bits<KR, LKR - LT, LKR>(acc);
+    elided_bar<T>(g);  // the inverse switch overwrites the buffer just read
 #pragma unroll
     for (int k = 0; k < KR; ++k) Z[idxB<Q, KR>(c, k) * 32 + lane] = acc[k];
     group_bar<T>(g);
@@ -857,14 +879,14 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
   long long lo, hi;
   group_range(ntask, (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
   // producer cursor over (task, unit) of this group
-  Cursor pc;
-  int pu = 0;
-  if (producer) pc.init(a, lo, hi, ncols);
+  UnitWalker pc;
+  if (producer) pc.init(a, lo, hi, ncols, lvl_begin);
   auto issue_next = [&](int k) {
     if (!pc.valid()) return;
-    if (sus_issue<Q, DMAX, MARKOV>(a, pc.fb, pc.item, pu, lvl_begin, sp.hdr + (size_t)k * kHdr,
-                                   sp.pay + (size_t)k * Sh::PAYA, sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k))
-      pc.advance(a);
+    const int fb = pc.fb;
+    const LvlUnit un = pc.take(a);
+    sus_issue_rec<Q, MARKOV>(a, fb, un, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA,
+                             sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k);
   };
   if (producer)
     for (int n = 0; n < S; ++n) issue_next(g * S + n);
@@ -967,6 +989,7 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       // reduction scratch lives in buffer 0.  Bulk mode reuses its buffers.
       // Phased mode needs none either (see sus_check_phased; red is in the stage).
       if constexpr (!SS::PHASED && (!SS::PP || SS::RED_D > (size_t)Q * 32)) group_bar<T>(g);
+      else elided_bar<T>(g);
     }
   }
 }

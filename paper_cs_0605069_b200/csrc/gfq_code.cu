@@ -90,10 +90,10 @@ int build_levels(const HostGraph &g, const int *order, bool chain, std::vector<i
     const int j = cols[k];
     const int e0 = g.col_ptr[j], dv = g.col_ptr[j + 1] - e0;
     lcol[k] = LvlCol{j, e0, dv, (int)lunit.size()};
-    if (dv == 0) lunit.push_back(LvlUnit{0, 0, 0, 0});
+    if (dv == 0) lunit.push_back(LvlUnit{0, 0, 0, 0, j, e0, 0, 0});
     for (int s = 0; s < dv; ++s) {
       const int e = g.col_edge[e0 + s], i = g.edge_check[e];
-      lunit.push_back(LvlUnit{g.row_ptr[i], g.row_ptr[i + 1] - g.row_ptr[i], e - g.row_ptr[i], i});
+      lunit.push_back(LvlUnit{g.row_ptr[i], g.row_ptr[i + 1] - g.row_ptr[i], e - g.row_ptr[i], i, j, e0, dv, s});
     }
   }
   return nlev;

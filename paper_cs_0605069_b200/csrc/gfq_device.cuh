@@ -147,6 +147,22 @@ __device__ __forceinline__ void group_bar(int g) {
     asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(T * 32) : "memory");
   }
 }
+// GFQ_SYNC_CHECK=1 builds the checking variant (libgfq_synccheck.so): a full
+// group barrier at every point where the default build elides one (one-sided
+// gathers, ping-pong and phased layout switches that reuse a buffer without a
+// barrier, no barrier between tasks).  Its outputs must be bit-identical to
+// the default build's (tests/test_gpu_sync_check.py) -- the race / sync check
+// of the barrier-elided kernels, compute-sanitizer being closed on this pool.
+#ifndef GFQ_SYNC_CHECK
+#define GFQ_SYNC_CHECK 0
+#endif
+template <int T>
+__device__ __forceinline__ void group_bar(int g);
+template <int T>
+__device__ __forceinline__ void elided_bar(int g) {
+  if constexpr (GFQ_SYNC_CHECK != 0 && T > 1) group_bar<T>(g);
+}
+
 // One-sided group barrier on a second id per group (15 - g; ids 1..G are the
 // group_bar ones): warp `waiter` waits until every other warp of the group has
 // arrived; the others only arrive and run on.  Safe to reuse because every
@@ -154,7 +170,7 @@ __device__ __forceinline__ void group_bar(int g) {
 template <int T>
 __device__ __forceinline__ void group_gather(int g, bool waiter) {
   if constexpr (T > 1) {
-    if (waiter)
+    if (GFQ_SYNC_CHECK != 0 || waiter)
       asm volatile("bar.sync %0, %1;" ::"r"(15 - g), "r"(T * 32) : "memory");
     else
       asm volatile("bar.arrive %0, %1;" ::"r"(15 - g), "r"(T * 32) : "memory");
@@ -606,6 +622,7 @@ __device__ __forceinline__ void vn_core(const WaveArgs &a, int fb, int j, const 
     if (k > 0) mx = fmax(mx, tot[k]);
   }
   if constexpr (T > 1 && ONEBAR) {
+    elided_bar<T>(g);  // red reused every other task without a barrier
 #pragma unroll
     for (int s = 0; s < NS; ++s) red[((size_t)s * T + c) * 32 + lane] = sums[s];
     red[((size_t)NS * T + c) * 32 + lane] = mx;
@@ -622,6 +639,7 @@ __device__ __forceinline__ void vn_core(const WaveArgs &a, int fb, int j, const 
     for (int cc = 1; cc < T; ++cc) mx = fmax(mx, red[((size_t)NS * T + cc) * 32 + lane]);
   } else if constexpr (T > 1) {
     // two-step cross-warp reduction: partials -> warp v reduces value v -> totals
+    elided_bar<T>(g);  // red reused across tasks without a barrier
 #pragma unroll
     for (int s = 0; s < NS; ++s) red[((size_t)s * T + c) * 32 + lane] = sums[s];
     red[((size_t)NS * T + c) * 32 + lane] = mx;
@@ -755,6 +773,13 @@ __device__ __forceinline__ void init_bars(uint64_t *bars, int T) {
 struct Cursor {
   long long t, hi;
   int fbi, item, fb, nitems;
+  // Prefetch the current item's edge range (row_ptr / col_ptr) into L1: the
+  // in-group producer lane reads it at its next refill, a task later (an L1
+  // hit), instead of stalling its warp -- and every barrier of its group -- on
+  // an L2 load right before the TMA issue.
+  __device__ __forceinline__ void load_range(const int *ptr) {
+    if (t < hi) asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr + item));
+  }
   __device__ __forceinline__ void init(const WaveArgs &a, long long t0, long long hi_, int nitems_) {
     t = t0;
     hi = hi_;
@@ -821,37 +846,89 @@ __device__ __forceinline__ void produce(const WaveArgs &a, uint64_t *bars, long 
 // ============================================================== SUS: stage issue
 // Units: one per (column, check slot) -- the check's other edges in at most
 // two contiguous runs; the last unit of a column also carries the prior's
-// extra rows and the column's VarDesc.
-template <int Q, int DMAX, bool MARKOV>
-__device__ __forceinline__ bool sus_issue(const WaveArgs &a, int fb, int col, int &s, int lvl_begin,
-                                          unsigned char *hdr, unsigned char *pay, unsigned char *xtra,
-                                          uint64_t *full) {
-  const LvlCol lc = a.c.lvl_col[lvl_begin + col];
-  const int nunits = lc.dv > 0 ? lc.dv : 1;
-  const LvlUnit un = a.c.lvl_unit[lc.unit0 + s];
+// extra rows and the column's VarDesc.  The unit's record (LvlUnit, level
+// order) comes from the producer's UnitWalker, which loads it one unit ahead:
+// no dependent global load on the producer lane between two TMA issues.
+template <int Q, bool MARKOV, bool XTRA_MARKOV = MARKOV>
+__device__ __forceinline__ void sus_issue_rec(const WaveArgs &a, int fb, const LvlUnit &un, unsigned char *hdr,
+                                              unsigned char *pay, unsigned char *xtra, uint64_t *full) {
   TaskInfo *ti = (TaskInfo *)hdr;
-  ti->fb = fb; ti->item = lc.j; ti->e0 = lc.e0; ti->deg = lc.dv;
-  ti->s = s; ti->r0 = un.r0; ti->d = un.d; ti->pos = un.pos; ti->i = un.i;
-  const bool last = (s == nunits - 1);
+  ti->fb = fb; ti->item = un.j; ti->e0 = un.e0; ti->deg = un.dv;
+  ti->s = un.s; ti->r0 = un.r0; ti->d = un.d; ti->pos = un.pos; ti->i = un.i;
+  const int nunits = un.dv > 0 ? un.dv : 1;
+  const bool last = (un.s == nunits - 1);
   uint32_t b0 = 0, b1 = 0;
   const float *rowbase = a.qmsg + ((size_t)fb * a.c.E + un.r0) * Q * 32;
-  if (lc.dv > 0) {
+  if (un.dv > 0) {
     b0 = (uint32_t)un.pos * Q * 128;
     b1 = (uint32_t)(un.d - 1 - un.pos) * Q * 128;
   }
-  const uint32_t bx = last ? 64 + extras_bytes<Q, MARKOV>(a, lc.j) : 0;
-  mbar_expect_tx(full, (lc.dv > 0 ? 64 + 32 : 0) + (a.early_exit ? 128 : 0) + b0 + b1 + bx);
-  if (lc.dv > 0) {
-    bulk_g2s(hdr + 128, a.c.sus_desc + lc.e0 + s, 64, full);
+  const uint32_t bx = last ? 64 + extras_bytes<Q, XTRA_MARKOV>(a, un.j) : 0;
+  mbar_expect_tx(full, (un.dv > 0 ? 64 + 32 : 0) + (a.early_exit ? 128 : 0) + b0 + b1 + bx);
+  if (un.dv > 0) {
+    bulk_g2s(hdr + 128, a.c.sus_desc + un.e0 + un.s, 64, full);
     bulk_g2s(hdr + 256, a.z + ((size_t)fb * a.c.M + un.i) * 32, 32, full);
   }
   if (a.early_exit) bulk_g2s(hdr + 384, a.conv + fb * 32, 128, full);
   if (b0) bulk_g2s(pay, rowbase, b0, full);
   if (b1) bulk_g2s(pay + (size_t)un.pos * Q * 128, rowbase + (size_t)(un.pos + 1) * Q * 32, b1, full);
   if (last) {
-    bulk_g2s(hdr + 192, a.c.var_desc + lc.j, 64, full);
-    issue_extras<Q, MARKOV>(a, fb, lc.j, xtra, full);
+    bulk_g2s(hdr + 192, a.c.var_desc + un.j, 64, full);
+    issue_extras<Q, XTRA_MARKOV>(a, fb, un.j, xtra, full);
   }
+}
+
+// Producer-side walk over the units of a contiguous range [lo, hi) of
+// (frame block, column) tasks of one level, in unit order (a level's units
+// are contiguous, column after column).  take() loads the current unit's
+// record (an L1 hit: it was prefetched when the previous unit was taken) and
+// prefetches the next one -- no dependent L2 load on the producer lane
+// between two TMA issues, and no record held in registers.
+struct UnitWalker {
+  long long t, hi;
+  int fbi, fb, col, ncols, u, u0;
+  __device__ __forceinline__ void init(const WaveArgs &a, long long lo, long long hi_, int ncols_, int lvl_begin) {
+    t = lo; hi = hi_; ncols = ncols_;
+    fbi = fb = col = u = u0 = 0;
+    if (t < hi) {
+      fbi = (int)(t / ncols);
+      col = (int)(t - (long long)fbi * ncols);
+      fb = a.list[fbi];
+      u0 = a.c.lvl_col[lvl_begin].unit0;
+      u = a.c.lvl_col[lvl_begin + col].unit0;
+    }
+  }
+  __device__ __forceinline__ bool valid() const { return t < hi; }
+  __device__ __forceinline__ LvlUnit take(const WaveArgs &a) {
+    const LvlUnit r = a.c.lvl_unit[u];
+    const bool col_done = r.s + 1 >= (r.dv > 0 ? r.dv : 1);
+    if (col_done) {
+      ++t;
+      if (++col == ncols) {
+        col = 0;
+        ++fbi;
+        if (t < hi) fb = a.list[fbi];
+        u = u0;
+      } else {
+        ++u;
+      }
+    } else {
+      ++u;
+    }
+    if (t < hi) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.c.lvl_unit + u));
+    return r;
+  }
+};
+
+template <int Q, int DMAX, bool MARKOV>
+__device__ __forceinline__ bool sus_issue(const WaveArgs &a, int fb, int col, int &s, int lvl_begin,
+                                          unsigned char *hdr, unsigned char *pay, unsigned char *xtra,
+                                          uint64_t *full) {
+  // generic-producer path (dedicated producer warp, produce()): loads the record
+  const LvlCol lc = a.c.lvl_col[lvl_begin + col];
+  const int nunits = lc.dv > 0 ? lc.dv : 1;
+  const LvlUnit un = a.c.lvl_unit[lc.unit0 + s];
+  sus_issue_rec<Q, MARKOV>(a, fb, un, hdr, pay, xtra, full);
   if (++s >= nunits) {
     s = 0;
     return true;  // task complete

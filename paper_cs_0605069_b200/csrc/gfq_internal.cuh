@@ -39,8 +39,9 @@ struct __align__(64) SusDesc {         // one per canonical edge (j, s) (SUS uni
 struct __align__(16) LvlCol {          // SUS level schedule, level order
   int j, e0, dv, unit0;                // column, its first canonical edge, degree, first unit
 };
-struct __align__(16) LvlUnit {         // one per (column, check slot) in level order
+struct __align__(32) LvlUnit {         // one per (column, check slot) in level order
   int r0, d, pos, i;                   // check row start / degree, position of e in the row, check
+  int j, e0, dv, s;                    // its column, the column's first canonical edge and degree, slot
 };
 static_assert(sizeof(CheckDesc) == 128 && sizeof(VarDesc) == 64 && sizeof(SusDesc) == 64, "desc sizes");
 

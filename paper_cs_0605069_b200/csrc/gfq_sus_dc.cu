@@ -33,13 +33,13 @@ namespace gfq {
 
 // warps per CTA / stages per warp (tuning knobs)
 #ifndef GFQ_DC_W
-#define GFQ_DC_W 8
+#define GFQ_DC_W 15
 #endif
 #ifndef GFQ_DC_S
-#define GFQ_DC_S 3
+#define GFQ_DC_S 1
 #endif
 #ifndef GFQ_DC_S_MARKOV
-#define GFQ_DC_S_MARKOV 3
+#define GFQ_DC_S_MARKOV 1
 #endif
 #ifndef GFQ_DC_FFMA2
 #define GFQ_DC_FFMA2 1
@@ -75,50 +75,19 @@ __device__ __forceinline__ void markov_rows(const WaveArgs &a, int fb, int j, co
   right = (nb & 2) ? a.qs_old + ((size_t)fb * N + (j + 1)) * Q * 32 : nullptr;
 }
 
-// One SUS unit (column, check slot) into a stage: as sus_issue (gfq_device.cuh),
-// with only the noise rows as extras; a Markov source column's neighbour
-// posteriors are prefetched into L2 with its first unit.
-template <int Q, int DMAX, bool MARKOV>
-__device__ __forceinline__ bool dc_issue(const WaveArgs &a, int fb, int col, int &s, int lvl_begin,
-                                         unsigned char *hdr, unsigned char *pay, unsigned char *xtra,
-                                         uint64_t *full) {
-  const LvlCol lc = a.c.lvl_col[lvl_begin + col];
-  const int nunits = lc.dv > 0 ? lc.dv : 1;
-  const LvlUnit un = a.c.lvl_unit[lc.unit0 + s];
-  TaskInfo *ti = (TaskInfo *)hdr;
-  ti->fb = fb; ti->item = lc.j; ti->e0 = lc.e0; ti->deg = lc.dv;
-  ti->s = s; ti->r0 = un.r0; ti->d = un.d; ti->pos = un.pos; ti->i = un.i;
-  const bool last = (s == nunits - 1);
-  if (MARKOV && s == 0 && lc.j < a.c.N) {
+// One SUS unit into a stage: sus_issue_rec (gfq_device.cuh) with only the
+// noise rows as extras; a Markov source column's neighbour posteriors are
+// prefetched into L2 with its first unit.
+template <int Q, bool MARKOV>
+__device__ __forceinline__ void dc_issue(const WaveArgs &a, int fb, const LvlUnit &un, unsigned char *hdr,
+                                         unsigned char *pay, unsigned char *xtra, uint64_t *full) {
+  if (MARKOV && un.s == 0 && un.j < a.c.N) {
     const float *l, *r;
-    markov_rows<Q>(a, fb, lc.j, l, r);
+    markov_rows<Q>(a, fb, un.j, l, r);
     if (l) prefetch_l2(l, Q * 128);
     if (r) prefetch_l2(r, Q * 128);
   }
-  uint32_t b0 = 0, b1 = 0;
-  const float *rowbase = a.qmsg + ((size_t)fb * a.c.E + un.r0) * Q * 32;
-  if (lc.dv > 0) {
-    b0 = (uint32_t)un.pos * Q * 128;
-    b1 = (uint32_t)(un.d - 1 - un.pos) * Q * 128;
-  }
-  const uint32_t bx = last ? 64 + extras_bytes<Q, false>(a, lc.j) : 0;
-  mbar_expect_tx(full, (lc.dv > 0 ? 64 + 32 : 0) + (a.early_exit ? 128 : 0) + b0 + b1 + bx);
-  if (lc.dv > 0) {
-    bulk_g2s(hdr + 128, a.c.sus_desc + lc.e0 + s, 64, full);
-    bulk_g2s(hdr + 256, a.z + ((size_t)fb * a.c.M + un.i) * 32, 32, full);
-  }
-  if (a.early_exit) bulk_g2s(hdr + 384, a.conv + fb * 32, 128, full);
-  if (b0) bulk_g2s(pay, rowbase, b0, full);
-  if (b1) bulk_g2s(pay + (size_t)un.pos * Q * 128, rowbase + (size_t)(un.pos + 1) * Q * 32, b1, full);
-  if (last) {
-    bulk_g2s(hdr + 192, a.c.var_desc + lc.j, 64, full);
-    issue_extras<Q, false>(a, fb, lc.j, xtra, full);
-  }
-  if (++s >= nunits) {
-    s = 0;
-    return true;
-  }
-  return false;
+  sus_issue_rec<Q, MARKOV, false>(a, fb, un, hdr, pay, xtra, full);
 }
 
 // u[y] = message(h^-1 y) for y = 0..Q-1 from a stage slot (fp32 rows of 32 lanes)
@@ -177,11 +146,12 @@ __device__ __forceinline__ void dc_conv(const float (&u)[Q], const float (&v)[Q]
 
 // SUS step 1 for one check of the column (DO = d-1 other edges): S in fp32,
 // then q * r_ij (the scale of the transform kernels' stored r, which the
-// variable node normalises away) into r slot ti.s of the warp.
-template <int Q, int DO, typename RF>
+// variable node normalises away) into r slot ti.s of the warp.  The stage is
+// released as soon as its rows are in registers; the caller refills it (one
+// copy of the issue code in the kernel: the instruction cache is the limit).
+template <int Q, int DO>
 __device__ __forceinline__ void dc_check(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_lane, uint32_t rt,
-                                         float *rsm, int lane, bool frozen, bool release, uint64_t *empty,
-                                         RF &&refill) {
+                                         float *rsm, int lane, bool frozen, bool release, uint64_t *empty) {
   const TaskInfo ti = *(const TaskInfo *)hdr;
   const SusDesc *sd = (const SusDesc *)(hdr + 128);
   const int z = hdr[256 + lane];
@@ -189,24 +159,24 @@ __device__ __forceinline__ void dc_check(const WaveArgs &a, const unsigned char 
   float S[Q];
   if constexpr (DO == 0) {
     // degree-1 check: the sum over no other variable is the point mass at 0
-    if (release) { release_stage(empty, lane); refill(); }
+    if (release) release_stage(empty, lane);
 #pragma unroll
     for (int y = 0; y < Q; ++y) S[y] = (y == 0) ? 1.0f : 0.0f;
   } else if constexpr (DO == 1) {
     dc_load<Q>(pay_lane, rt, sd->perm_o[0], S);
-    if (release) { release_stage(empty, lane); refill(); }
+    if (release) release_stage(empty, lane);
   } else {
     float u[Q], v[Q];
     dc_load<Q>(pay_lane, rt, sd->perm_o[0], u);
     dc_load<Q>(pay_lane + Q * 128, rt, sd->perm_o[1], v);
     if constexpr (DO == 2) {
-      if (release) { release_stage(empty, lane); refill(); }
+      if (release) release_stage(empty, lane);
       dc_conv<Q>(u, v, S);
     } else {
       static_assert(DO == 3, "dc_check: check degree <= 4");
       float w[Q], t[Q];
       dc_load<Q>(pay_lane + 2 * Q * 128, rt, sd->perm_o[2], w);
-      if (release) { release_stage(empty, lane); refill(); }
+      if (release) release_stage(empty, lane);
       dc_conv<Q>(u, v, t);
       dc_conv<Q>(t, w, S);
     }
@@ -227,29 +197,100 @@ __device__ __forceinline__ void dc_check(const WaveArgs &a, const unsigned char 
 }
 
 // SUS step 2 (+ step 4, reading A8) for the column: Eq. (4) for each of its
-// edges and the posterior Eq. (5) with clipping, from the fresh r's.
-template <int Q, int DV, bool MARKOV>
-__device__ __forceinline__ void dc_vn(const WaveArgs &a, const unsigned char *hdr, const unsigned char *xtra,
-                                      const float *Tsm, const float *rsm, int lane, bool frozen) {
+// edges and the posterior Eq. (5) with clipping, from the fresh r's (fp32 rows
+// of the warp's r slots) and the prior (an fp32 row computed once, dc_prior).
+// fp64 products and sums as vn_core, streamed over the entries in two passes
+// (sums, then normalised stores): few registers and little code, so more
+// warps fit an SM and the kernel stays in the instruction cache.
+template <int Q>
+__device__ __forceinline__ void dc_prior(const WaveArgs &a, int fb, int j, const unsigned char *xtra,
+                                         const float *Tsm, float *prs, int lane) {
+  double pr[Q];
+  if (a.markov && j < a.c.N) {
+    const float *l, *r;
+    markov_rows<Q>(a, fb, j, l, r);   // L2-resident (prefetched with the column's first unit)
+    prior_from<Q, Q, true>(a, j, 0, lane, l ? l : r, Tsm, pr, r ? r : l);
+  } else {
+    prior_from<Q, Q, false>(a, j, 0, lane, (const float *)xtra, Tsm, pr);
+  }
+#pragma unroll
+  for (int k = 0; k < Q; ++k) prs[k * 32 + lane] = (float)pr[k];
+}
+
+template <int Q, int DV>
+__device__ __forceinline__ void dc_vn(const WaveArgs &a, const unsigned char *hdr, const float *rsm,
+                                      const float *prs, int lane, bool frozen) {
+  constexpr int NS = DV + 1;
   const TaskInfo ti = *(const TaskInfo *)hdr;
   const VarDesc *vd = (const VarDesc *)(hdr + 192);
-  int qdst[DV > 0 ? DV : 1];
-  double r[DV > 0 ? DV : 1][Q];
+  const int fb = ti.fb, j = ti.item;
+  const long long E = a.c.E;
+  const float *P = prs + lane;
+  const float *R = rsm + lane;
+  // leave-one-out products at entry k: o[s] = p prod_{s' != s} r_s', o[DV] = p prod r
+  auto prods = [&](int k, double (&o)[NS]) {
+    const double p = (double)P[k * 32];
+    double r[DV > 0 ? DV : 1];
 #pragma unroll
-  for (int s = 0; s < DV; ++s) {
-    qdst[s] = vd->qdst[s];
+    for (int t = 0; t < DV; ++t) r[t] = (double)R[(t * Q + k) * 32];
+    if constexpr (DV == 0) {
+      o[0] = p;
+    } else if constexpr (DV == 1) {
+      o[0] = p; o[1] = p * r[0];
+    } else if constexpr (DV == 2) {
+      o[0] = p * r[1]; o[1] = p * r[0]; o[2] = o[0] * r[0];
+    } else {
+      const double x = p * r[0], bc = r[1] * r[2];
+      o[0] = p * bc; o[1] = x * r[2]; o[2] = x * r[1]; o[3] = x * bc;
+    }
+  };
+  double sums[NS], mx = 0.0;
 #pragma unroll
-    for (int k = 0; k < Q; ++k) r[s][k] = (double)rsm[((size_t)s * Q + k) * 32 + lane];
+  for (int t = 0; t < NS; ++t) sums[t] = 0.0;
+#pragma unroll 2
+  for (int k = 0; k < Q; ++k) {
+    double o[NS];
+    prods(k, o);
+#pragma unroll
+    for (int t = 0; t < NS; ++t) sums[t] += o[t];
+    mx = fmax(mx, o[DV]);
   }
-  double pr[Q];
-  if (MARKOV && ti.item < a.c.N) {
-    const float *l, *r;
-    markov_rows<Q>(a, ti.fb, ti.item, l, r);   // L2-resident (prefetched with the first unit)
-    prior_from<Q, Q, MARKOV>(a, ti.item, 0, lane, l ? l : r, Tsm, pr, r ? r : l);
-  } else {
-    prior_from<Q, Q, MARKOV>(a, ti.item, 0, lane, (const float *)xtra, Tsm, pr);
+  int bad = 0;
+  double inv[NS];
+  float add[NS];
+#pragma unroll
+  for (int t = 0; t < NS; ++t) {
+    const bool ok = sums[t] > 0.0 && isfinite(sums[t]);
+    bad += !ok;
+    inv[t] = ok ? fast_rcp(sums[t]) : 0.0;
+    add[t] = ok ? 0.0f : 1.0f / Q;
   }
-  vn_core<Q, Q, DV, MARKOV, false>(a, ti.fb, ti.item, qdst, r, pr, nullptr, 0, 0, lane, frozen);
+  const bool okq = add[DV] == 0.0f;
+  const double thr = mx * (1.0 - kTieRel);  // clipping: smallest a within the tie band
+  int bidx = Q;
+  float *qrow[DV > 0 ? DV : 1];
+#pragma unroll
+  for (int t = 0; t < DV; ++t) qrow[t] = a.qmsg + ((size_t)fb * E + vd->qdst[t]) * Q * 32 + lane;
+  float *qsrow = (a.markov && j < a.c.N && a.qs_new) ? a.qs_new + ((size_t)fb * a.c.N + j) * Q * 32 + lane : nullptr;
+  float *qarow = a.qall ? a.qall + ((size_t)fb * a.c.V + j) * Q * 32 + lane : nullptr;
+#pragma unroll 2
+  for (int k = 0; k < Q; ++k) {
+    double o[NS];
+    prods(k, o);
+    if (o[DV] >= thr && bidx == Q) bidx = k;
+    if (!frozen) {
+#pragma unroll
+      for (int t = 0; t < DV; ++t) qrow[t][k * 32] = (float)(o[t] * inv[t]) + add[t];
+      const float qv = (float)(o[DV] * inv[DV]) + add[DV];
+      if (qsrow) qsrow[k * 32] = qv;
+      if (qarow) qarow[k * 32] = qv;
+    }
+  }
+  if (bidx >= Q || !okq) bidx = 0;
+  if (!frozen) {
+    a.xhat[((size_t)fb * a.c.V + j) * 32 + lane] = (unsigned char)bidx;
+    if (bad) atomicAdd(a.stats + 0, (unsigned long long)bad);
+  }
 }
 
 template <int Q, int DMAX, int DVMAX, bool MARKOV, int S, int W>
@@ -280,14 +321,14 @@ __global__ void __launch_bounds__(DCShape<Q, DMAX, DVMAX, MARKOV, S, W>::THREADS
   const bool producer = (lane == 0);
   long long lo, hi;
   group_range(ntask, (long long)blockIdx.x * W + g, (long long)gridDim.x * W, lo, hi);
-  Cursor pc;
-  int pu = 0;
-  if (producer) pc.init(a, lo, hi, ncols);
+  UnitWalker pc;
+  if (producer) pc.init(a, lo, hi, ncols, lvl_begin);
   auto issue_next = [&](int k) {
     if (!pc.valid()) return;
-    if (dc_issue<Q, DMAX, MARKOV>(a, pc.fb, pc.item, pu, lvl_begin, sp.hdr + (size_t)k * kHdr,
-                                   sp.pay + (size_t)k * Sh::PAYA, sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k))
-      pc.advance(a);
+    const int fb = pc.fb;
+    const LvlUnit un = pc.take(a);
+    dc_issue<Q, MARKOV>(a, fb, un, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA,
+                        sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k);
   };
   if (producer)
     for (int n = 0; n < S; ++n) issue_next(g * S + n);
@@ -318,23 +359,28 @@ __global__ void __launch_bounds__(DCShape<Q, DMAX, DVMAX, MARKOV, S, W>::THREADS
         // the last unit's stage also carries the column's VarDesc and prior
         // rows: it is released after the variable update
         switch (d - 1) {
-          case 0: dc_check<Q, 0>(a, hdr, pay_lane, rt, rsm, lane, frozen, !last, empty, refill); break;
-          case 1: dc_check<Q, 1>(a, hdr, pay_lane, rt, rsm, lane, frozen, !last, empty, refill); break;
-          case 2: dc_check<Q, 2>(a, hdr, pay_lane, rt, rsm, lane, frozen, !last, empty, refill); break;
-          default: dc_check<Q, 3>(a, hdr, pay_lane, rt, rsm, lane, frozen, !last, empty, refill); break;
+          case 0: dc_check<Q, 0>(a, hdr, pay_lane, rt, rsm, lane, frozen, !last, empty); break;
+          case 1: dc_check<Q, 1>(a, hdr, pay_lane, rt, rsm, lane, frozen, !last, empty); break;
+          case 2: dc_check<Q, 2>(a, hdr, pay_lane, rt, rsm, lane, frozen, !last, empty); break;
+          default: dc_check<Q, 3>(a, hdr, pay_lane, rt, rsm, lane, frozen, !last, empty); break;
         }
       }
       if (last) {
-        __syncwarp();  // the column's r slots are complete
+        // the prior row goes to this stage's payload: its rows are in registers
+        // already, and the stage is released only after the variable update
+        float *prs = (float *)(sp.pay + (size_t)k * Sh::PAYA);
+        static_assert(Sh::PAYA >= (size_t)Q * 128, "prior row fits a stage payload");
+        dc_prior<Q>(a, ti->fb, ti->item, xtra, Tsm, prs, lane);
+        __syncwarp();  // the column's r slots and prior row are complete
         switch (dv) {
-          case 0: dc_vn<Q, 0, MARKOV>(a, hdr, xtra, Tsm, rsm, lane, frozen); break;
-          case 1: dc_vn<Q, 1, MARKOV>(a, hdr, xtra, Tsm, rsm, lane, frozen); break;
-          case 2: dc_vn<Q, 2, MARKOV>(a, hdr, xtra, Tsm, rsm, lane, frozen); break;
-          default: dc_vn<Q, 3, MARKOV>(a, hdr, xtra, Tsm, rsm, lane, frozen); break;
+          case 0: dc_vn<Q, 0>(a, hdr, rsm, prs, lane, frozen); break;
+          case 1: dc_vn<Q, 1>(a, hdr, rsm, prs, lane, frozen); break;
+          case 2: dc_vn<Q, 2>(a, hdr, rsm, prs, lane, frozen); break;
+          default: dc_vn<Q, 3>(a, hdr, rsm, prs, lane, frozen); break;
         }
         release_stage(empty, lane);  // syncwarp: every lane is done with the r slots too
-        refill();
       }
+      refill();  // the stage was released above (last unit) or in dc_check
     }
   }
 }

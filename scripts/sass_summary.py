@@ -1,9 +1,12 @@
-"""Compact SASS summary of an ncu report: instruction mix and top stall lines.
-usage: sass_summary.py REPORT [kernel-regex]"""
+"""Compact SASS summary of an ncu report (or its exported source-page CSV):
+instruction mix and top stall lines.  usage: sass_summary.py REPORT|CSV"""
 import collections, csv, io, subprocess, sys
 rep = sys.argv[1]
-args = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"]
-txt = subprocess.run(args, capture_output=True, text=True).stdout
+if rep.endswith(".csv"):          # an exported `--page source --csv --print-source sass`
+    txt = open(rep).read()
+else:
+    args = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"]
+    txt = subprocess.run(args, capture_output=True, text=True).stdout
 lines = txt.splitlines()
 # a report may hold several kernels: blocks start with "Kernel Name"
 blocks, cur = [], []

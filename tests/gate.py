@@ -17,13 +17,38 @@ from __future__ import annotations
 import numpy as np
 
 TIE_ALLOW = 1e-5
+GPU_TIE = 1e-6        # the kernels' own clipping band (gfq_device.cuh kTieRel, reading A17)
 GATE_LOG: list = []   # rows printed by conftest.pytest_terminal_summary
 
 
-def decision_gate(gpu_x, gpu_it, ref_x, ref_it, oracle_Q_for=None):
+def clip_band(Q, band: float = GPU_TIE):
+    """The GPU's clipping rule applied to posteriors Q [n][q]: the smallest a whose
+    value is within `band` (relative) of the maximum (reading A17)."""
+    Q = np.asarray(Q)
+    return np.argmax(Q >= Q.max(-1, keepdims=True) * (1.0 - band), axis=-1).astype(np.uint8)
+
+
+def tie_rule_replay(Q_at, unsat, t_from: int, t_to: int, band: float = GPU_TIE):
+    """Replay the convergence test with the GPU's tie rule on the ORACLE's fp64
+    posteriors: for t = t_from..t_to, x = clip_band(Q^(t)); the first t with
+    H x = z.  Clipping never feeds back into the messages, so this is
+    the oracle's decode with the GPU's decision rule.  Q_at(t) -> Q [V][q];
+    unsat(x) -> violated checks.  Returns (t or -1, x of that t / the last)."""
+    x = None
+    for t in range(t_from, t_to + 1):
+        x = clip_band(Q_at(t), band)
+        if unsat(x) == 0:
+            return t, x
+    return -1, x
+
+
+def decision_gate(gpu_x, gpu_it, ref_x, ref_it, oracle_Q_for=None, replay=None):
     """gpu_x/ref_x [F][n] symbols, gpu_it/ref_it [F].  oracle_Q_for(frame_idx) ->
     (x [k][n], Q [k][n][q]): the oracle's final estimate and posterior for those
     frames (only called for frames that converge at the same t with different x).
+    replay(f, t_gpu, t_ref) -> (t, x_src) of tie_rule_replay for a frame whose
+    convergence iteration differs: it matches when the oracle's messages with
+    the GPU's tie rule stop at the GPU's iteration with the GPU's estimate.
     Returns (match [F] bool, strict [F] bool, n_allowance)."""
     gpu_x, ref_x = np.asarray(gpu_x), np.asarray(ref_x)
     gpu_it, ref_it = np.asarray(gpu_it), np.asarray(ref_it)
@@ -44,7 +69,33 @@ def decision_gate(gpu_x, gpu_it, ref_x, ref_it, oracle_Q_for=None):
             if np.all(got >= Q.max(-1) * (1.0 - TIE_ALLOW)):
                 match[f] = True
                 n_allow += 1
+    if replay is not None:
+        for f in np.where(~match & (gpu_it != ref_it))[0][:8]:
+            t, x = replay(int(f), int(gpu_it[f]), int(ref_it[f]))
+            if t == int(gpu_it[f]) and (t == -1 or np.array_equal(x, gpu_x[f])):
+                match[f] = True
+                n_allow += 1
     return match, strict, n_allow
+
+
+def oracle_replay(oc, hard, pi, N: int, max_iters: int, **kw):
+    """replay() for decision_gate from an oracle.OCode and the frames' evidence
+    (hard [F][M p], pi [F][M p]): per-t posteriors by fixed-iteration decodes."""
+    p = oc.p
+
+    def replay(f, t_gpu, t_ref):
+        h1, p1 = hard[f:f + 1], pi[f:f + 1]
+        rsym = (h1.reshape(-1, p).astype(np.int64) << np.arange(p)).sum(1)
+        z = oc.syndrome(rsym.astype(np.uint8))
+        lo = min(t for t in (t_gpu, t_ref) if t > 0) if (t_gpu > 0 or t_ref > 0) else max_iters
+        hi = max_iters if min(t_gpu, t_ref) < 0 else max(t_gpu, t_ref)
+        hi = min(hi, lo + 6)
+
+        def Q_at(t):
+            return oc.decode(h1, p1, max_iters=t, fixed=True, keep_messages=True, threads=1, **kw)["Q"][0]
+        t, x = tie_rule_replay(Q_at, lambda x: oc.unsatisfied(x, z), lo, hi)
+        return t, (None if x is None else x[:N])
+    return replay
 
 
 def record(case: str, F: int, match, strict, n_allow, extra: str = "") -> int:

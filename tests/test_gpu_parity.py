@@ -82,9 +82,9 @@ def _oracle_Q(oc, hard, pi, N, **kw):
     return f
 
 
-def _decision_match(gpu_x, gpu_it, ref_x, ref_it, oracle_Q_for=None, case=None):
+def _decision_match(gpu_x, gpu_it, ref_x, ref_it, oracle_Q_for=None, case=None, replay=None):
     """Reading A18 plus the fp32 tie allowance (tests/gate.py)."""
-    match, strict, n_allow = gate.decision_gate(gpu_x, gpu_it, ref_x, ref_it, oracle_Q_for)
+    match, strict, n_allow = gate.decision_gate(gpu_x, gpu_it, ref_x, ref_it, oracle_Q_for, replay)
     if case:
         gate.record(case, len(match), match, strict, n_allow)
     return match, strict
@@ -149,7 +149,8 @@ def test_full_size_sampled(gfq, name, full):
         ref = oc.decode(hard, pi, schedule=schedule, max_iters=cfg.max_iters, T=T)
         match, _ = _decision_match(s_hat[sample], iters[sample], ref["xhat"][:, :code.N], ref["iters"],
                                    _oracle_Q(oc, hard, pi, code.N, schedule=schedule, max_iters=cfg.max_iters, T=T),
-                                   "full-size sample %s %s" % (name, "SUS" if schedule else "PUS"))
+                                   "full-size sample %s %s" % (name, "SUS" if schedule else "PUS"),
+                                   gate.oracle_replay(oc, hard, pi, code.N, cfg.max_iters, schedule=schedule, T=T))
         assert match.all()
 
 
