@@ -361,8 +361,17 @@ def decode_run(args, cfg, F, iters, schedules, steps, warmup, gfq, shard, dist, 
             pc = gfq.Params(ch, param, s, cfg.max_iters, early_exit=True, markov_T=T)
             sh, ic, _ = gfq.gfq_decode(gcode, obs_c, pc, workspace=ws, stream=stream)   # warm-up
             c_ms = timer(lambda: gfq.gfq_decode(gcode, obs_c, pc, sh, ic, ws, stream))
+            blk_it = gfq.gfq_decode_stats(gcode, ws)["block_iterations"]
             its[s] = ic.cpu().numpy()
             errs = (sh.cpu().numpy() != truth[:nf]).any(axis=1)
+            # the same decode with block-granular compaction only (a block runs
+            # until its slowest frame stops): what frame-granular compaction saves
+            pb = gfq.Params(ch, param, s, cfg.max_iters, early_exit=True, markov_T=T,
+                            compaction=gfq.GFQ_COMPACT_BLOCKS)
+            shb, icb, _ = gfq.gfq_decode(gcode, obs_c, pb, workspace=ws, stream=stream)
+            b_ms = timer(lambda: gfq.gfq_decode(gcode, obs_c, pb, shb, icb, ws, stream))
+            blk_it_b = gfq.gfq_decode_stats(gcode, ws)["block_iterations"]
+            same = bool(torch.equal(sh, shb) and torch.equal(ic, icb))
             # per-iteration time at this batch: a fixed 10-iteration decode of the same frames
             pf = gfq.Params(ch, param, s, 10, early_exit=False, markov_T=T)
             f_ms = timer(lambda: gfq.gfq_decode(gcode, obs_c, pf, sh, ic, ws, stream)) / 10.0
@@ -372,7 +381,11 @@ def decode_run(args, cfg, F, iters, schedules, steps, warmup, gfq, shard, dist, 
                               nonconverged=int((~ok).sum()), frame_error_rate=float(errs.mean()),
                               ms_to_converge=c_ms, ms_per_iteration_full_batch=f_ms,
                               ideal_ms=float(spent.mean() * f_ms),
-                              measured_over_ideal=float(c_ms / (spent.mean() * f_ms)))
+                              measured_over_ideal=float(c_ms / (spent.mean() * f_ms)),
+                              block_iterations=int(blk_it), ideal_block_iterations=float(spent.sum() / 32.0),
+                              block_granular=dict(ms_to_converge=b_ms, block_iterations=int(blk_it_b),
+                                                  measured_over_ideal=float(b_ms / (spent.mean() * f_ms)),
+                                                  outputs_identical=same))
         if len(schedules) == 2:
             both = (its[schedules[0]] > 0) & (its[schedules[1]] > 0)
             if both.any():

@@ -47,6 +47,7 @@ extern "C" {
 typedef enum { GFQ_BSC = 0, GFQ_BEC = 1, GFQ_BIAWGN = 2 } gfq_channel;
 typedef enum { GFQ_PUS = 0, GFQ_SUS = 1 } gfq_schedule;
 typedef enum { GFQ_PRIOR_SNAPSHOT = 0, GFQ_PRIOR_IN_SWEEP = 1 } gfq_prior_update;
+typedef enum { GFQ_COMPACT_FRAMES = 0, GFQ_COMPACT_BLOCKS = 1 } gfq_compaction;
 
 /* Opaque, immutable after creation; may be shared by concurrent decodes on
  * different streams (each with its own workspace). */
@@ -113,6 +114,21 @@ typedef struct {
      * any order, A6) or with GFQ_PRIOR_IN_SWEEP (defined along index order). */
     const int *sus_order;
     int sus_n_orders;
+    /* Early-exit compaction (a frame stops at its first passing
+     * test; early_exit = 1 only).  Frames are decoded 32 to a block, one per
+     * lane, and a block keeps iterating until its slowest frame stops:
+     *   GFQ_COMPACT_FRAMES (0, default): when enough lanes have gone idle, the
+     *     still-decoding frames of the sparsest blocks are moved (messages,
+     *     evidence, syndrome, estimate, posterior snapshot) into the idle
+     *     lanes of the others, so the blocks that keep iterating stay full;
+     *   GFQ_COMPACT_BLOCKS (1): only blocks whose frames have all stopped are
+     *     dropped.
+     * A frame's arithmetic does not depend on its lane or on the other frames
+     * of its block, so both settings give bit-identical s_hat / iters; they
+     * differ in stats[1] (block iterations executed) and in time.  Ignored
+     * (blocks) with keep_messages = 1, whose export addresses frames by their
+     * original lane.  GFQ_EINVAL for other values. */
+    int compaction;
 } gfq_params;
 
 /* Thread-local description of the last error (never NULL). */
@@ -264,7 +280,7 @@ int gfq_simulate(const gfq_code *code, int n_frames, unsigned long long seed, lo
  * duration in ms (ms[k]) and the number of launches (launches[k]); NULL outputs
  * are skipped.  gfq_kernel_name(k) names kind k ("cn", "vn", "sus", ...) or
  * returns NULL for k out of range. */
-#define GFQ_NKERNELS 14
+#define GFQ_NKERNELS 15
 int gfq_profile_enable(int on);
 int gfq_profile_read(double *ms, long long *launches);
 const char *gfq_kernel_name(int kind);

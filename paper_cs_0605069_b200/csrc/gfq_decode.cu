@@ -64,6 +64,8 @@ Layout make_layout(const gfq_code *c, int fbw, const gfq_params *prm) {
   L.newconv = take(F32 * sizeof(int));
   L.active = take((size_t)fbw * sizeof(int));
   L.list = take((size_t)fbw * sizeof(int));
+  L.fid = take(F32 * sizeof(int));
+  L.rp = take(repack_plan_bytes(fbw));
   L.total = off;
   return L;
 }
@@ -118,6 +120,10 @@ static int check_params(const gfq_code *c, const gfq_params *prm, bool need_chan
       }
     }
   }
+  if (prm->compaction != GFQ_COMPACT_FRAMES && prm->compaction != GFQ_COMPACT_BLOCKS) {
+    set_error("bad compaction");
+    return GFQ_EINVAL;
+  }
   if ((prm->trace == nullptr) != (prm->trace_truth == nullptr)) {
     set_error("trace and trace_truth must both be set or both be NULL");
     return GFQ_EINVAL;
@@ -152,10 +158,10 @@ static T *at(void *ws, size_t off) {
 
 // ---------------------------------------------------------------- profiling
 enum Kind { K_FRONTEND, K_SYNDROME, K_INIT_MSGS, K_INIT_STATE, K_CN, K_VN, K_SUS, K_TEST, K_FINALIZE,
-            K_CAPTURE, K_COMPACT, K_CLIP, K_OTHER, K_TRACE, K_N };
+            K_CAPTURE, K_COMPACT, K_CLIP, K_OTHER, K_TRACE, K_REPACK, K_N };
 static const char *kKindNames[K_N] = {"frontend", "syndrome", "init_msgs", "init_state", "cn", "vn",
                                       "sus", "test", "finalize", "capture", "compact", "clip", "other",
-                                      "trace"};
+                                      "trace", "repack"};
 static_assert(K_N == GFQ_NKERNELS, "kernel kinds");
 
 struct Profiler {
@@ -332,6 +338,7 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
     a.active = at<int>(ws, L.active);
     a.list = at<int>(ws, L.list);
     a.nactive = at<int>(ws, L.nactive);
+    a.fid = at<int>(ws, L.fid);
     a.stats = at<unsigned long long>(ws, L.stats);
     a.T = prm->markov_T ? at<double>(ws, L.T) : nullptr;
     a.Tf = prm->markov_T ? at<float>(ws, L.Tf) : nullptr;
@@ -355,6 +362,8 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
     const std::vector<int> &lptr = a.gs ? c->level_ptr_gs_h : c->level_ptr_h;
     const int nlev = a.gs ? c->n_levels_gs : c->n_levels;
     a.early_exit = prm->early_exit ? 1 : 0;
+    const bool repack = a.early_exit && !prm->keep_messages && prm->compaction == GFQ_COMPACT_FRAMES && a.nfb > 1;
+    const RepackPlan rp = repack_plan_at(at<char>(ws, L.rp), fbw);
     a.t = 1;
     float *qs[2] = {at<float>(ws, L.qs0), at<float>(ws, L.qs1)};
 
@@ -408,6 +417,10 @@ static int decode_common(const gfq_code *c, int F, int mode, double ch_param, co
       RUN(K_TEST, launch_test(a, st));
       RUN(K_FINALIZE, launch_finalize(a, 0, st));
       RUN(K_CAPTURE, launch_capture(a, out, Lout, 0, st));
+      // frame-granular compaction: fill the idle lanes of the live blocks with
+      // the frames of the sparsest ones (which k_compact then drops); the
+      // snapshot the next iteration reads moves with them
+      if (repack && t < prm->max_iters) RUN(K_REPACK, launch_repack(a, rp, a.qs_new, st));
       RUN(K_COMPACT, launch_compact(a, st));
       if (a.early_exit && ring.ok) {
         const int k = (t - 1) % LagRing::K;

@@ -108,7 +108,27 @@ struct Layout {
   int fbw;            // frame blocks per wave
   size_t qmsg, rmsg, pi, hard, z, xhat, qs0, qs1, qall, iters, conv, unsat, newconv;
   size_t active, list, nactive, stats, T, Tf, pi0, ord_col, ord_unit, total;
+  size_t fid, rp;     // lane slot -> frame of the wave; frame-compaction plan (RepackPlan header + tables)
 };
+
+// Frame-granular early-exit compaction (gfq_kernels.cu: k_repack_plan,
+// k_repack_move): the plan of one round, in the workspace.
+//   [0] n_dst  [1] blocks before  [2] blocks after  [3] frames moved
+// followed by dst[fbw] (destination block of plan entry k), map[fbw*32]
+// (entry k, lane l: source slot block*32+lane, or -1 = keep), and scratch.
+struct RepackPlan {
+  int *hdr;       // [4]
+  int *dst;       // [fbw]
+  int *map;       // [fbw*32]
+  int *cnt;       // [fbw]  live index -> number of still-decoding frames
+  unsigned *amask;  // [fbw]  live index -> their lanes
+  int *role;      // [fbw]  live index -> 1 donor, 0 receiver
+  int *dpre;      // [fbw+1] donor index -> frames in the donors before it
+  int *dblk;      // [fbw]  donor index -> live index
+  int *rpre;      // [fbw]  live index -> idle lanes in the receivers before it
+};
+size_t repack_plan_bytes(int fbw);
+RepackPlan repack_plan_at(void *base, int fbw);
 Layout make_layout(const gfq_code *c, int fbw, const gfq_params *prm);
 
 // -------------------------------------------------------------- kernel args
@@ -132,6 +152,7 @@ struct WaveArgs {
   int *active;          // [nfb]
   int *list;            // [nfb] active block ids (wave-local)
   int *nactive;         // [1]
+  int *fid;             // [nfb*32] frame of the wave decoded in this lane slot, -1 = none
   unsigned long long *stats;  // [4]
   const double *T;      // [q*q] or null
   const float *Tf;      // [2*q*q] fp32 copies of T (row-major) and of T^T, or null
@@ -159,6 +180,9 @@ int launch_test(const WaveArgs &a, cudaStream_t s);
 int launch_finalize(const WaveArgs &a, int final_pass, cudaStream_t s);
 int launch_capture(const WaveArgs &a, unsigned char *out, int L, int mode, cudaStream_t s);
 int launch_compact(const WaveArgs &a, cudaStream_t s);
+// frame-granular compaction: plan (which frames move where) and move; qs = the
+// posterior snapshot the next iteration reads (or null)
+int launch_repack(const WaveArgs &a, const RepackPlan &rp, float *qs, cudaStream_t s);
 int launch_clip_priors(const WaveArgs &a, cudaStream_t s);
 int launch_export(const WaveArgs &a, float *q_out, float *r_out, float *Q_out, cudaStream_t s);
 int launch_set_u64(unsigned long long *p, unsigned long long v, cudaStream_t s);

@@ -124,6 +124,7 @@ __global__ void k_init_state(WaveArgs a) {
     const long long gf = (long long)a.fb0 * 32 + f;
     const bool valid = gf < a.n_frames;
     a.iters[f] = -1;
+    a.fid[f] = valid ? f : -1;
     a.conv[f] = valid ? 0 : 1;
     a.unsat[f] = 0;
     a.newconv[f] = 0;
@@ -173,7 +174,7 @@ __global__ void k_finalize(WaveArgs a, int final_pass) {
       nc = (a.conv[f] == 0);
     } else if (a.active[f >> 5] && a.conv[f] == 0 && a.unsat[f] == 0) {
       a.conv[f] = 1;
-      a.iters[f] = a.t;
+      a.iters[a.fid[f]] = a.t;  // by frame: the lane slot may hold a moved frame (k_repack_plan)
       nc = 1;
       atomicAdd(a.stats + 2, 1ull);
     }
@@ -198,7 +199,7 @@ __global__ void k_capture(WaveArgs a, unsigned char *out, int L) {
   __syncthreads();
   for (int fl = warp; fl < 32; fl += 4) {
     if (!((mask >> fl) & 1)) continue;
-    const long long f = (long long)(a.fb0 + fb) * 32 + fl;
+    const long long f = (long long)a.fb0 * 32 + a.fid[fb * 32 + fl];  // flagged slots hold a frame
     for (int r = lane; r < 128; r += 32) {
       const int j = j0 + r;
       if (j < L) out[f * L + j] = tile[r][fl];
@@ -249,6 +250,217 @@ __global__ void k_compact(WaveArgs a, unsigned int *host_count) {
   }
 }
 
+
+// ============================================================== frame-granular early-exit compaction
+// A block iterates until its slowest frame has stopped, so late in
+// a decode most lanes of the live blocks are idle.  One round, after the
+// estimates of the frames that stopped in this iteration have been captured:
+// k_repack_plan picks the D = B - ceil(A/32) sparsest of the B live blocks
+// (A = frames still decoding) as donors and assigns their frames, in order, to
+// the idle lanes of the other live blocks (receivers), when D >= 1 and
+// 3 D >= ceil(A/32) (moving a frame costs about one iteration of its bytes);
+// k_repack_move then copies the per-frame rows (q messages, per-bit evidence,
+// syndrome, estimate, posterior snapshot) lane to lane.  The donors are left
+// with no decoding frame and k_compact drops them.  A frame's arithmetic does
+// not depend on its lane, so the decode's outputs do not change.
+__device__ __forceinline__ int cta_excl_scan(int v, int *wsum, int &total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  int off = 0, tot = 0;
+  for (int w = 0; w < nw; ++w) {
+    const int sw = wsum[w];
+    if (w < warp) off += sw;
+    tot += sw;
+  }
+  __syncthreads();
+  total = tot;
+  return off + x - v;
+}
+
+__global__ void __launch_bounds__(1024) k_repack_plan(WaveArgs a, RepackPlan rp) {
+  __shared__ int hist[33];
+  __shared__ int wsum[32];
+  __shared__ int s_cstar, s_neq, s_go, s_ndst;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int B = *a.nactive;
+  if (tid < 33) hist[tid] = 0;
+  if (tid == 0) s_ndst = 0;
+  __syncthreads();
+  for (int i = warp; i < B; i += nw) {
+    const int b = a.list[i];
+    const unsigned m = __ballot_sync(0xffffffffu, a.conv[b * 32 + lane] == 0);
+    if (lane == 0) {
+      rp.cnt[i] = __popc(m);
+      rp.amask[i] = m;
+      atomicAdd(&hist[__popc(m)], 1);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int A = 0;
+    for (int c = 1; c <= 32; ++c) A += c * hist[c];
+    const int need = (A + 31) / 32;
+    const int D = B - need;              // donors, the blocks with no frame left included
+    const int Dn = D - hist[0];          // donors that still hold frames
+    const int go = (Dn >= 1 && 3 * Dn >= need) ? 1 : 0;
+    int less = 0, cstar = 0;
+    for (; cstar <= 32; ++cstar) {
+      if (less + hist[cstar] > D) break;
+      less += hist[cstar];
+    }
+    s_cstar = cstar;     // donors: every block with fewer frames than cstar ...
+    s_neq = D - less;    // ... and the first s_neq blocks (list order) with exactly cstar
+    s_go = go;
+    rp.hdr[0] = 0;
+    rp.hdr[1] = B;
+    rp.hdr[2] = go ? need : B;
+    rp.hdr[3] = 0;
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const int cstar = s_cstar, neq = s_neq;
+  // roles
+  int carry = 0;
+  for (int i0 = 0; i0 < B; i0 += blockDim.x) {
+    const int i = i0 + tid;
+    const int c = i < B ? rp.cnt[i] : 33;
+    int tot;
+    const int rank = carry + cta_excl_scan(c == cstar ? 1 : 0, wsum, tot);
+    carry += tot;
+    if (i < B) rp.role[i] = (c < cstar || (c == cstar && rank < neq)) ? 1 : 0;
+  }
+  __syncthreads();
+  // donor index / frames before each donor; idle lanes before each receiver
+  int cd = 0, cf = 0, cr = 0;
+  for (int i0 = 0; i0 < B; i0 += blockDim.x) {
+    const int i = i0 + tid;
+    const int role = i < B ? rp.role[i] : -1;
+    const int c = i < B ? rp.cnt[i] : 0;
+    int t0, t1, t2;
+    const int di = cd + cta_excl_scan(role == 1 ? 1 : 0, wsum, t0);
+    const int df = cf + cta_excl_scan(role == 1 ? c : 0, wsum, t1);
+    const int rf = cr + cta_excl_scan(role == 0 ? 32 - c : 0, wsum, t2);
+    cd += t0; cf += t1; cr += t2;
+    if (role == 1) {
+      rp.dblk[di] = i;
+      rp.dpre[di] = df;
+    } else if (role == 0) {
+      rp.rpre[i] = rf;
+    }
+  }
+  const int nd = cd, adon = cf;
+  if (tid == 0) rp.dpre[nd] = adon;
+  __syncthreads();
+  // receivers take the donors' frames in order
+  for (int i = warp; i < B; i += nw) {
+    if (rp.role[i] != 0) continue;                 // warp-uniform
+    const unsigned fm = ~rp.amask[i];
+    const int o = rp.rpre[i];
+    if (o >= adon || fm == 0u) continue;
+    const int b = a.list[i];
+    int src = -1;
+    if ((fm >> lane) & 1u) {
+      const int idx = o + __popc(fm & ((1u << lane) - 1u));
+      if (idx < adon) {
+        int lo = 0, hi = nd;                       // largest d with dpre[d] <= idx < dpre[d+1]
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (rp.dpre[mid] <= idx) lo = mid; else hi = mid;
+        }
+        const int li = rp.dblk[lo];
+        const int sl = __fns(rp.amask[li], 0, idx - rp.dpre[lo] + 1);
+        src = a.list[li] * 32 + sl;
+      }
+    }
+    int k = 0;
+    if (lane == 0) k = atomicAdd(&s_ndst, 1);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    if (lane == 0) rp.dst[k] = b;
+    rp.map[k * 32 + lane] = src;
+    if (src >= 0) {
+      const int slot = b * 32 + lane;
+      a.fid[slot] = a.fid[src];
+      a.conv[slot] = 0;
+      a.fid[src] = -1;
+      a.conv[src] = 1;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    rp.hdr[0] = s_ndst;
+    rp.hdr[3] = adon;
+  }
+}
+
+struct MoveSet {
+  void *base[5];
+  long long rows[5];   // rows per block
+  int esz[5];          // bytes per lane: 4 (float rows of 128 B) or 1 (byte rows of 32 B)
+  int n;
+};
+
+__device__ __forceinline__ float shfl_lane(float v, int l) { return __shfl_sync(0xffffffffu, v, l); }
+__device__ __forceinline__ unsigned char shfl_lane(unsigned char v, int l) {
+  return (unsigned char)__shfl_sync(0xffffffffu, (int)v, l);
+}
+
+template <typename T, int U>
+__device__ __forceinline__ void move_rows(T *base, long long rows, const RepackPlan &rp, int nd, long long w0,
+                                          long long nwarps, int lane) {
+  const long long per = (rows + U - 1) / U;
+  const long long ntask = (long long)nd * per;
+  for (long long task = w0; task < ntask; task += nwarps) {
+    const int k = (int)(task / per);
+    const long long r0 = (task - (long long)k * per) * U;
+    const int db = rp.dst[k];
+    const int src = rp.map[k * 32 + lane];
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (r0 + u < rows) v[u] = base[((size_t)db * rows + r0 + u) * 32 + lane];
+    unsigned todo = __ballot_sync(0xffffffffu, src >= 0);
+    while (todo) {
+      const int leader = __ffs(todo) - 1;
+      const int sb = __shfl_sync(0xffffffffu, src, leader) >> 5;
+      const bool mine = src >= 0 && (src >> 5) == sb;
+      T w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (r0 + u < rows) w[u] = base[((size_t)sb * rows + r0 + u) * 32 + lane];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (r0 + u < rows) {
+          const T pick = shfl_lane(w[u], src & 31);
+          if (mine) v[u] = pick;
+        }
+      }
+      todo &= ~__ballot_sync(0xffffffffu, mine);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (r0 + u < rows) base[((size_t)db * rows + r0 + u) * 32 + lane] = v[u];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_repack_move(RepackPlan rp, MoveSet ms) {
+  const int nd = rp.hdr[0];
+  if (nd == 0) return;
+  const int lane = threadIdx.x & 31;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int ai = 0; ai < ms.n; ++ai) {
+    if (ms.esz[ai] == 4) move_rows<float, 4>((float *)ms.base[ai], ms.rows[ai], rp, nd, w0, nwarps, lane);
+    else move_rows<unsigned char, 4>((unsigned char *)ms.base[ai], ms.rows[ai], rp, nd, w0, nwarps, lane);
+  }
+}
+
 __global__ void k_set_u64(unsigned long long *p, unsigned long long v) { *p = v; }
 
 // ============================================================== Fig. 1 instrumentation
@@ -266,13 +478,13 @@ __global__ void k_trace(WaveArgs a, const unsigned char *truth, int *trace, int 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int N = a.c.N, p = a.c.p;
   const unsigned mask = (1u << p) - 1u;
-  const long long f0 = (long long)(a.fb0 + fb) * 32;
+  const long long f0 = (long long)a.fb0 * 32;
   int ok = 0;
   for (int j0 = w * 32; j0 < N; j0 += 8 * 32) {
     for (int r = 0; r < 32; ++r) {
-      const long long f = f0 + r;
+      const int fl = a.fid[fb * 32 + r];  // the frame in lane slot r (-1: none)
       const int j = j0 + lane;
-      tile[w][r][lane] = (f < a.n_frames && j < N) ? truth[f * N + j] : 0;
+      tile[w][r][lane] = (fl >= 0 && j < N) ? truth[(f0 + fl) * N + j] : 0;
     }
     __syncwarp();
     const int jn = min(32, N - j0);
@@ -287,8 +499,8 @@ __global__ void k_trace(WaveArgs a, const unsigned char *truth, int *trace, int 
   if (w == 0) {
     int s = 0;
     for (int k = 0; k < 8; ++k) s += part[k][lane];
-    const long long f = f0 + lane;
-    if (f < a.n_frames) trace[f * tlen + t] = s;
+    const int fl = a.fid[fb * 32 + lane];
+    if (fl >= 0) trace[(f0 + fl) * tlen + t] = s;
   }
 }
 
@@ -373,6 +585,48 @@ int launch_capture(const WaveArgs &a, unsigned char *out, int L, int /*mode*/, c
 int launch_compact(const WaveArgs &a, cudaStream_t s) {
   k_compact<<<1, 1024, 0, s>>>(a, nullptr);
   return check_launch("k_compact");
+}
+
+size_t repack_plan_bytes(int fbw) {
+  const size_t n = (size_t)fbw;
+  // hdr[64] dst[n] map[32n] cnt[n] amask[n] role[n] dpre[n+1] dblk[n] rpre[n]
+  return (64 + n * 32 + n * 7 + 1 + 63) * sizeof(int);
+}
+
+RepackPlan repack_plan_at(void *base, int fbw) {
+  RepackPlan rp;
+  int *p = (int *)base;
+  const size_t n = (size_t)fbw;
+  rp.hdr = p; p += 64;
+  rp.map = p; p += n * 32;
+  rp.dst = p; p += n;
+  rp.cnt = p; p += n;
+  rp.amask = (unsigned *)p; p += n;
+  rp.role = p; p += n;
+  rp.dpre = p; p += n + 1;
+  rp.dblk = p; p += n;
+  rp.rpre = p;
+  return rp;
+}
+
+int launch_repack(const WaveArgs &a, const RepackPlan &rp, float *qs, cudaStream_t s) {
+  k_repack_plan<<<1, 1024, 0, s>>>(a, rp);
+  int rc = check_launch("k_repack_plan");
+  if (rc) return rc;
+  MoveSet ms;
+  int n = 0;
+  auto add = [&](void *base, long long rows, int esz) {
+    if (base && rows > 0) { ms.base[n] = base; ms.rows[n] = rows; ms.esz[n] = esz; ++n; }
+  };
+  add(a.qmsg, a.c.E * a.c.q, 4);
+  add(a.pi, (long long)a.c.M * a.c.p, 4);
+  add(qs, (long long)a.c.N * a.c.q, 4);
+  add(a.z, a.c.M, 1);
+  add(a.xhat, a.c.V, 1);
+  ms.n = n;
+  for (int k = n; k < 5; ++k) { ms.base[k] = nullptr; ms.rows[k] = 0; ms.esz[k] = 4; }
+  k_repack_move<<<sm_count() * 8, 256, 0, s>>>(rp, ms);
+  return check_launch("k_repack_move");
 }
 
 int launch_export(const WaveArgs &a, float *q_out, float *r_out, float *Q_out, cudaStream_t s) {

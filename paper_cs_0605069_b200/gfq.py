@@ -20,13 +20,14 @@ GFQ_OK, GFQ_EINVAL, GFQ_ENOMEM, GFQ_ECUDA, GFQ_EUNSUPPORTED = 0, -1, -2, -3, -4
 GFQ_BSC, GFQ_BEC, GFQ_BIAWGN = 0, 1, 2
 GFQ_PUS, GFQ_SUS = 0, 1
 GFQ_PRIOR_SNAPSHOT, GFQ_PRIOR_IN_SWEEP = 0, 1
+GFQ_COMPACT_FRAMES, GFQ_COMPACT_BLOCKS = 0, 1
 
 # Every symbol declared in include/gfq.h (checked by tests/test_abi.py).
 EXPORTS = ["gfq_last_error", "gfq_version", "gfq_code_create", "gfq_code_destroy", "gfq_code_info",
            "gfq_workspace_bytes", "gfq_decode", "gfq_decode_evidence", "gfq_workspace_bytes_host",
            "gfq_decode_host", "gfq_export_messages", "gfq_decode_stats", "gfq_profile_enable",
            "gfq_profile_read", "gfq_kernel_name", "gfq_simulate_workspace_bytes", "gfq_simulate"]
-GFQ_NKERNELS = 14
+GFQ_NKERNELS = 15
 
 
 class GfqError(RuntimeError):
@@ -42,7 +43,7 @@ class gfq_params(ctypes.Structure):
                 ("src_pi0", ctypes.c_void_p), ("keep_messages", ctypes.c_int),
                 ("trace_truth", ctypes.c_void_p), ("trace", ctypes.c_void_p),
                 ("prior_update", ctypes.c_int), ("sus_order", ctypes.c_void_p),
-                ("sus_n_orders", ctypes.c_int)]
+                ("sus_n_orders", ctypes.c_int), ("compaction", ctypes.c_int)]
 
 
 class gfq_sim_params(ctypes.Structure):
@@ -147,7 +148,8 @@ class Params:
 
     def __init__(self, channel=GFQ_BSC, ch_param=0.0, schedule=GFQ_PUS, max_iters=100,
                  early_exit=True, markov_T=None, src_pi0=None, keep_messages=False,
-                 trace_truth=None, trace=None, prior_update=GFQ_PRIOR_SNAPSHOT, sus_order=None):
+                 trace_truth=None, trace=None, prior_update=GFQ_PRIOR_SNAPSHOT, sus_order=None,
+                 compaction=GFQ_COMPACT_FRAMES):
         """trace_truth / trace: CUDA tensors uint8 [F][N] and int32 [F][max_iters+1]
         (Fig. 1 instrumentation, see include/gfq.h), or None."""
         self._T = None if markov_T is None else np.ascontiguousarray(markov_T, dtype=np.float64)
@@ -161,7 +163,8 @@ class Params:
                             int(bool(keep_messages)), _dptr(trace_truth), _dptr(trace),
                             int(prior_update),
                             None if self._ord is None else self._ord.ctypes.data,
-                            0 if self._ord is None else int(self._ord.shape[0]))
+                            0 if self._ord is None else int(self._ord.shape[0]),
+                            int(compaction))
 
     def ref(self):
         return ctypes.byref(self.c)
