@@ -1,6 +1,6 @@
 /*
  * gfq.h -- C ABI of libgfq: batched belief-propagation decoding of
- * MacKay-Neal codes over GF(2^p) (q = 2^p = 2..128) on one NVIDIA B200.
+ * MacKay-Neal codes over GF(2^p) (q = 2^p = 2..256) on one NVIDIA B200.
  *
  * Method: Yacov, Efraim, Kfir, Kanter, Shental, "Parallel vs. Sequential
  * Belief Propagation Decoding of LDPC Codes over GF(q) and Markov Sources"
@@ -42,7 +42,7 @@ extern "C" {
 #define GFQ_EINVAL (-1)       /* bad argument (see each call)                  */
 #define GFQ_ENOMEM (-2)       /* host or device allocation failed (create only) */
 #define GFQ_ECUDA (-3)        /* CUDA runtime error (message has the details)   */
-#define GFQ_EUNSUPPORTED (-4) /* valid but not implemented (p > 7, degree > 8)   */
+#define GFQ_EUNSUPPORTED (-4) /* valid but not implemented (p > 8, degree > 8)   */
 
 typedef enum { GFQ_BSC = 0, GFQ_BEC = 1, GFQ_BIAWGN = 2 } gfq_channel;
 typedef enum { GFQ_PUS = 0, GFQ_SUS = 1 } gfq_schedule;
@@ -149,7 +149,7 @@ int gfq_version(void);
  * to the encoder (Eq. 1) only.
  * Errors: GFQ_EINVAL for p < 1, N < 0, M < 1, a polynomial that is not
  * primitive of degree p, an index out of range, a value 0 or >= q, or a
- * duplicate (row, col); GFQ_EUNSUPPORTED for p > 7 or a check/variable degree
+ * duplicate (row, col); GFQ_EUNSUPPORTED for p > 8 or a check/variable degree
  * > 8; GFQ_ENOMEM / GFQ_ECUDA from allocation or upload.  *out is set only on
  * success. */
 int gfq_code_create(gfq_code **out, int p, unsigned prim_poly, int N, int M,

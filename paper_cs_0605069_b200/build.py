@@ -5,7 +5,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgfq.so")
-SOURCES = ["gfq_code.cu", "gfq_kernels.cu", "gfq_bp.cu", "gfq_sus_dc.cu", "gfq_decode.cu", "gfq_sim.cu"]
+SOURCES = ["gfq_code.cu", "gfq_kernels.cu", "gfq_bp.cu", "gfq_sus_dc.cu", "gfq_bigq.cu", "gfq_decode.cu", "gfq_sim.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr", "--extended-lambda",

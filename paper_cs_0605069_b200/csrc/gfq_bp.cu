@@ -1116,24 +1116,28 @@ static int sus_q(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
 }
 
 int launch_cn(const WaveArgs &a, cudaStream_t s) {
+  if (big_applies(a)) return launch_big_cn(a, s);
 #define F(Q) cn_q<Q>(a, s)
   GFQ_DISPATCH_Q(a.c.q, F)
 #undef F
 }
 
 int launch_vn(const WaveArgs &a, cudaStream_t s) {
+  if (big_applies(a)) return launch_big_vn(a, 0, s);
 #define F(Q) vn_q<Q>(a, 0, s)
   GFQ_DISPATCH_Q(a.c.q, F)
 #undef F
 }
 
 int launch_clip_priors(const WaveArgs &a, cudaStream_t s) {
+  if (big_applies(a)) return launch_big_vn(a, 1, s);
 #define F(Q) vn_q<Q>(a, 1, s)
   GFQ_DISPATCH_Q(a.c.q, F)
 #undef F
 }
 
 int launch_sus_level(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
+  if (big_applies(a)) return launch_big_sus(a, lb, ncols, s);
 #define F(Q) sus_q<Q>(a, lb, ncols, s)
   GFQ_DISPATCH_Q(a.c.q, F)
 #undef F

@@ -113,7 +113,7 @@ extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int 
                                const int *B_row, const int *B_col,
                                const unsigned char *B_val) {
   if (!out) { set_error("gfq_code_create: out is NULL"); return GFQ_EINVAL; }
-  if (p > 7) { set_error("gfq_code_create: p > 7 unsupported"); return GFQ_EUNSUPPORTED; }
+  if (p > 8) { set_error("gfq_code_create: p > 8 unsupported"); return GFQ_EUNSUPPORTED; }
   if (p < 1 || N < 0 || M < 1 || nnzA < 0 || nnzB < 0) {
     set_error("gfq_code_create: bad sizes");
     return GFQ_EINVAL;

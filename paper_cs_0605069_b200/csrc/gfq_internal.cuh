@@ -176,6 +176,10 @@ int launch_vn(const WaveArgs &a, cudaStream_t s);
 int launch_sus_level(const WaveArgs &a, int level, int ncols, cudaStream_t s);
 bool sus_dc_applies(const WaveArgs &a);   // gfq_sus_dc.cu
 int launch_sus_dc(const WaveArgs &a, int level, int ncols, cudaStream_t s);
+bool big_applies(const WaveArgs &a);      // gfq_bigq.cu: q = 256
+int launch_big_cn(const WaveArgs &a, cudaStream_t s);
+int launch_big_vn(const WaveArgs &a, int clip_only, cudaStream_t s);
+int launch_big_sus(const WaveArgs &a, int level, int ncols, cudaStream_t s);
 int launch_test(const WaveArgs &a, cudaStream_t s);
 int launch_finalize(const WaveArgs &a, int final_pass, cudaStream_t s);
 int launch_capture(const WaveArgs &a, unsigned char *out, int L, int mode, cudaStream_t s);

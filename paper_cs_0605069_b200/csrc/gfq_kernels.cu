@@ -544,6 +544,8 @@ int launch_syndrome(const WaveArgs &a, cudaStream_t s) {
   const int threads = 256;
   const long long tasks = (long long)a.nfb * a.c.M;
   const int grid = (int)std::max<long long>(1, std::min<long long>((tasks + 7) / 8, (long long)sm_count() * 8));
+  if (a.c.q * a.c.q > 48 * 1024)
+    cudaFuncSetAttribute(k_syndrome, cudaFuncAttributeMaxDynamicSharedMemorySize, a.c.q * a.c.q);
   k_syndrome<<<grid, threads, a.c.q * a.c.q, s>>>(a);
   return check_launch("k_syndrome");
 }
@@ -566,6 +568,8 @@ int launch_test(const WaveArgs &a, cudaStream_t s) {
   const int threads = 256;
   const long long tasks = (long long)a.nfb * ((a.c.M + chunk - 1) / chunk);
   const int grid = (int)std::max<long long>(1, std::min<long long>((tasks + 7) / 8, (long long)sm_count() * 8));
+  if (a.c.q * a.c.q > 48 * 1024)
+    cudaFuncSetAttribute(k_test, cudaFuncAttributeMaxDynamicSharedMemorySize, a.c.q * a.c.q);
   k_test<<<grid, threads, a.c.q * a.c.q, s>>>(a, chunk);
   return check_launch("k_test");
 }

@@ -199,10 +199,16 @@ int launch_sim(const SimArgs &a, cudaStream_t s) {
   const int q = a.c.q;
   const int nthr = a.nfb * 32;
   const size_t smem_src = a.markov ? sizeof(double) * (size_t)(q + q * q) : 0;
+  if (smem_src > 227 * 1024) {
+    set_error("gfq_simulate: the Markov source tables of this field size do not fit in shared memory");
+    return GFQ_EUNSUPPORTED;
+  }
   if (smem_src > 48 * 1024) cudaFuncSetAttribute(k_sim_source, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_src);
   k_sim_source<<<(nthr + 127) / 128, 128, smem_src, s>>>(a);
   int rc = check_launch("k_sim_source");
   if (rc) return rc;
+  if ((size_t)q * q + q > 48 * 1024)
+    cudaFuncSetAttribute(k_sim_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, q * q + q);
   k_sim_encode<<<(a.nfb + 3) / 4, 128, (size_t)q * q + q, s>>>(a);
   if ((rc = check_launch("k_sim_encode"))) return rc;
   if (a.s_out) {

@@ -44,7 +44,7 @@ def test_gf_large_fields_sampled(p):
         assert oracle.gf_mul(a, oracle.gf_inv(a, p, POLY[p]), p, POLY[p]) == 1
 
 
-@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
 def test_gf_primitive_element_order(p):
     """x generates the multiplicative group: ord(x) = q-1 (the polynomials are primitive, A1)."""
     q = 1 << p
@@ -138,7 +138,7 @@ def brute_check(p, h, qin, z, out):
 
 @pytest.mark.parametrize("p,d", [(1, 1), (1, 2), (1, 3), (1, 4), (2, 2), (2, 3), (2, 4),
                                  (3, 2), (3, 3), (3, 4), (4, 2), (4, 3), (6, 2), (6, 3),
-                                 (7, 2), (7, 3)])
+                                 (7, 2), (7, 3), (8, 2)])
 def test_check_node_equals_enumeration(p, d):
     q = 1 << p
     rng = np.random.default_rng(100 * p + d)
@@ -151,6 +151,27 @@ def test_check_node_equals_enumeration(p, d):
             r = oracle.check_node(p, POLY[p], h, qin, z, out)
             assert np.max(np.abs(r - brute_check(p, h, qin, z, out))) < 1e-12
             assert abs(r.sum() - 1) < 1e-12           # exact normalisation (reading A5)
+
+
+def test_check_node_equals_enumeration_gf256_degree3():
+    """Eq. (3) at q = 256, d = 3: every configuration (x1, x2) of the two other
+    variables enumerated at once (numpy), summed into the symbol a they force."""
+    p, q = 8, 256
+    mul = synth.gf_tables(p).mul
+    rng = np.random.default_rng(808)
+    h = rng.integers(1, q, 3)
+    qin = rng.random((3, q)) + 1e-3
+    qin /= qin.sum(1, keepdims=True)
+    z = int(rng.integers(q))
+    for out in range(3):
+        o1, o2 = [k for k in range(3) if k != out]
+        y = mul[h[o1], np.arange(q)][:, None] ^ mul[h[o2], np.arange(q)][None, :]   # h1 x1 + h2 x2
+        S = np.zeros(q)
+        np.add.at(S, y.ravel(), np.outer(qin[o1], qin[o2]).ravel())
+        r_enum = np.array([S[z ^ int(mul[h[out], a])] for a in range(q)])          # h_out a = z + (...)
+        r = oracle.check_node(p, POLY[p], h, qin, z, out)
+        assert np.max(np.abs(r - r_enum)) < 1e-12
+        assert abs(r.sum() - 1) < 1e-12
 
 
 def test_check_node_worked_values(golden):
