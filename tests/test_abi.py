@@ -61,7 +61,7 @@ def _create(gfq, p=2, poly=0x7, N=2, M=2, A=((0, 0, 1), (1, 1, 2)), B=((0, 0, 1)
 
 
 def test_create_validation(gfq):
-    assert _create(gfq, p=8, poly=0x11D)[0] == gfq.GFQ_EUNSUPPORTED      # q = 256 (f4: q <= 128)
+    assert _create(gfq, p=9, poly=0x211)[0] == gfq.GFQ_EUNSUPPORTED      # q = 512 (f4: q <= 256)
     assert _create(gfq, poly=0xB)[0] == gfq.GFQ_EINVAL                    # wrong degree
     assert _create(gfq, p=4, poly=0x1F)[0] == gfq.GFQ_EINVAL              # irreducible, not primitive
     assert _create(gfq, A=((0, 0, 4),))[0] == gfq.GFQ_EINVAL              # value >= q
