@@ -5,7 +5,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgfq.so")
-SOURCES = ["gfq_code.cu", "gfq_kernels.cu", "gfq_bp.cu", "gfq_sus_dc.cu", "gfq_bigq.cu", "gfq_decode.cu", "gfq_sim.cu"]
+SOURCES = ["gfq_code.cu", "gfq_kernels.cu", "gfq_bp.cu", "gfq_sus_dc.cu", "gfq_sus_dc64.cu", "gfq_bigq.cu", "gfq_decode.cu", "gfq_sim.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr", "--extended-lambda",
@@ -58,7 +58,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
 
 
 SYNC_CHECK_LIB = os.path.join(HERE, "libgfq_synccheck.so")
-KERNEL_SOURCES = ("gfq_bp.cu", "gfq_sus_dc.cu")   # the ones GFQ_SYNC_CHECK changes
+KERNEL_SOURCES = ("gfq_bp.cu", "gfq_sus_dc.cu", "gfq_sus_dc64.cu")   # the ones GFQ_SYNC_CHECK changes
 
 
 def build_sync_check(force: bool = False) -> str:

@@ -1109,6 +1109,7 @@ static int sus_launch(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
 template <int Q>
 static int sus_q(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
   if (GFQ_SUS_DC && sus_dc_applies(a)) return launch_sus_dc(a, lb, ncols, s);
+  if (sus_dc64_applies(a)) return launch_sus_dc64(a, lb, ncols, s);
   const bool small = a.c.max_cdeg <= 4 && a.c.max_vdeg <= 3;
   if (a.markov)
     return small ? sus_launch<Q, 4, 3, true>(a, lb, ncols, s) : sus_launch<Q, 8, 8, true>(a, lb, ncols, s);

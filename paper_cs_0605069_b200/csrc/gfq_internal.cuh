@@ -176,6 +176,8 @@ int launch_vn(const WaveArgs &a, cudaStream_t s);
 int launch_sus_level(const WaveArgs &a, int level, int ncols, cudaStream_t s);
 bool sus_dc_applies(const WaveArgs &a);   // gfq_sus_dc.cu
 int launch_sus_dc(const WaveArgs &a, int level, int ncols, cudaStream_t s);
+bool sus_dc64_applies(const WaveArgs &a); // gfq_sus_dc64.cu: q = 64 by direct convolution
+int launch_sus_dc64(const WaveArgs &a, int level, int ncols, cudaStream_t s);
 bool big_applies(const WaveArgs &a);      // gfq_bigq.cu: q = 256
 int launch_big_cn(const WaveArgs &a, cudaStream_t s);
 int launch_big_vn(const WaveArgs &a, int clip_only, cudaStream_t s);

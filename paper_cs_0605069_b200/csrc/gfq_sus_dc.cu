@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "gfq_device.cuh"
 #include "gfq_launch.cuh"
 
@@ -417,13 +419,26 @@ static int dc_launch(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
   return check_launch("k_sus_dc");
 }
 
-// Fields handled here: q = 16 (check degree <= 4, variable degree <= 3).
+// Fields handled here: q = 16 (check degree <= 4, variable degree <= 3); the
+// environment variable GFQ_SUS_DC_MINQ (4 or 8) extends it to smaller fields
+// (measurement: the transform kernel has no layout switches there either).
+#ifndef GFQ_SUS_DC_MINQ_DEFAULT
+#define GFQ_SUS_DC_MINQ_DEFAULT 16
+#endif
 bool sus_dc_applies(const WaveArgs &a) {
-  return a.c.q == 16 && a.c.max_cdeg <= 4 && a.c.max_vdeg <= 3;
+  static int minq = -1;
+  if (minq < 0) {
+    const char *e = getenv("GFQ_SUS_DC_MINQ");
+    minq = e ? atoi(e) : GFQ_SUS_DC_MINQ_DEFAULT;
+    if (minq < 4) minq = 4;
+  }
+  return a.c.q >= minq && a.c.q <= 16 && a.c.max_cdeg <= 4 && a.c.max_vdeg <= 3;
 }
 
 int launch_sus_dc(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
   switch (a.c.q) {
+    case 4: return a.markov ? dc_launch<4, true>(a, lb, ncols, s) : dc_launch<4, false>(a, lb, ncols, s);
+    case 8: return a.markov ? dc_launch<8, true>(a, lb, ncols, s) : dc_launch<8, false>(a, lb, ncols, s);
     case 16: return a.markov ? dc_launch<16, true>(a, lb, ncols, s) : dc_launch<16, false>(a, lb, ncols, s);
     default: break;
   }
