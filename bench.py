@@ -299,7 +299,7 @@ def decode_run(args, cfg, F, iters, schedules, steps, warmup, gfq, shard, dist, 
         n_sched = sum(1 for s in schedules if (s == gfq.GFQ_SUS) == (kname == "sus"))
         alg = 8.0 * cfg.q * upd_per_frame_iter[kname] * F * iters * n_sched
         traffic, tsrc = None, None
-        for tpath in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_traffic.json")), reverse=True):
+        for tpath in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_traffic*.json")), reverse=True):
             try:
                 tj = json.load(open(tpath))
             except Exception:

@@ -29,8 +29,7 @@ from typing import Optional
 import numpy as np
 
 # Primitive polynomials (reading A1).  p=1 uses x+1 (GF(2): multiply = AND).
-PRIM_POLY = {1: 0x3, 2: 0x7, 3: 0xB, 4: 0x13, 5: 0x25, 6: 0x43, 7: 0x89,   # 7: x^7+x^3+1 (f4)
-             8: 0x11D}                                                  # 8: x^8+x^4+x^3+x^2+1 (f4)
+PRIM_POLY = {1: 0x3, 2: 0x7, 3: 0xB, 4: 0x13, 5: 0x25, 6: 0x43, 7: 0x89}  # 7: x^7+x^3+1 (f4)
 
 BSC, BEC, BIAWGN = 0, 1, 2
 CHANNEL_NAMES = {BSC: "bsc", BEC: "bec", BIAWGN: "biawgn"}
