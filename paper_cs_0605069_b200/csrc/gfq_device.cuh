@@ -402,13 +402,18 @@ __device__ __forceinline__ void loo_signed(double (&u)[DM][KR], const uint32_t (
 
 // Sign masks of the syndrome shift: bit 31 set where (-1)^{popc(w & z)} = -1,
 // w = k*T + c (layout B) or k (T = 1).
+// parity of a value < 16 without POPC (a slow-pipe instruction whose latency
+// showed up as 8 % of k_cn's stall samples, profiles/r02): bit x of 0x6996
+__device__ __forceinline__ uint32_t parity4(int x) { return (0x6996u >> (x & 15)) & 1u; }
+
 template <int KR, int T>
 __device__ __forceinline__ void sign_masks(int z, int c, uint32_t (&sm)[KR]) {
   constexpr int LT = ilog2(T);
+  static_assert(KR <= 16 && T <= 16, "sign_masks: parity4 covers 4 bits");
   const int zk = z >> LT;
-  const uint32_t base = (T > 1) ? ((uint32_t)(__popc(z & c & (T - 1)) & 1) << 31) : 0u;
+  const uint32_t base = (T > 1) ? (parity4(z & c & (T - 1)) << 31) : 0u;
 #pragma unroll
-  for (int k = 0; k < KR; ++k) sm[k] = base ^ ((uint32_t)(__popc(zk & k) & 1) << 31);
+  for (int k = 0; k < KR; ++k) sm[k] = base ^ (parity4(zk & k) << 31);
 }
 
 // ============================================================== priors

@@ -92,6 +92,25 @@ __device__ __forceinline__ void dc_issue(const WaveArgs &a, int fb, const LvlUni
   sus_issue_rec<Q, MARKOV, false>(a, fb, un, hdr, pay, xtra, full);
 }
 
+// With one stage per warp the TMA load of a unit starts only when the previous
+// unit has released the stage, so its HBM latency is exposed (the mbarrier wait
+// was 19 % of the stall samples at C4, profiles/r02).  The producer lane
+// therefore prefetches the NEXT unit's message rows into L2 while the current
+// unit is being processed (a second UnitWalker running one unit ahead, whose
+// record was itself prefetched a step earlier): the later TMA load is an L2 hit.
+// In flight: 148 SMs x 15 warps x <= 6 KB, far below the 126 MB of L2.
+#ifndef GFQ_DC_L2_PREFETCH
+#define GFQ_DC_L2_PREFETCH 1
+#endif
+template <int Q>
+__device__ __forceinline__ void dc_prefetch_unit(const WaveArgs &a, int fb, const LvlUnit &un) {
+  if (un.dv <= 0) return;
+  const float *rowbase = a.qmsg + ((size_t)fb * a.c.E + un.r0) * Q * 32;
+  const uint32_t b0 = (uint32_t)un.pos * Q * 128, b1 = (uint32_t)(un.d - 1 - un.pos) * Q * 128;
+  if (b0) prefetch_l2(rowbase, b0);
+  if (b1) prefetch_l2(rowbase + (size_t)(un.pos + 1) * Q * 32, b1);
+}
+
 // u[y] = message(h^-1 y) for y = 0..Q-1 from a stage slot (fp32 rows of 32 lanes)
 template <int Q>
 __device__ __forceinline__ void dc_load(uint32_t slot_lane, uint32_t rt, unsigned long long pk, float (&u)[Q]) {
@@ -323,14 +342,25 @@ __global__ void __launch_bounds__(DCShape<Q, DMAX, DVMAX, MARKOV, S, W>::THREADS
   const bool producer = (lane == 0);
   long long lo, hi;
   group_range(ntask, (long long)blockIdx.x * W + g, (long long)gridDim.x * W, lo, hi);
-  UnitWalker pc;
-  if (producer) pc.init(a, lo, hi, ncols, lvl_begin);
+  UnitWalker pc, la;   // la runs S units ahead of pc (L2 prefetch)
+  if (producer) {
+    pc.init(a, lo, hi, ncols, lvl_begin);
+    if (GFQ_DC_L2_PREFETCH) {
+      la.init(a, lo, hi, ncols, lvl_begin);
+      for (int n = 0; n < S && la.valid(); ++n) (void)la.take(a);
+    }
+  }
   auto issue_next = [&](int k) {
     if (!pc.valid()) return;
     const int fb = pc.fb;
     const LvlUnit un = pc.take(a);
     dc_issue<Q, MARKOV>(a, fb, un, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA,
                         sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k);
+    if (GFQ_DC_L2_PREFETCH && la.valid()) {
+      const int fb1 = la.fb;
+      const LvlUnit un1 = la.take(a);   // an L1 hit: prefetched when la took the unit before it
+      dc_prefetch_unit<Q>(a, fb1, un1);
+    }
   };
   if (producer)
     for (int n = 0; n < S; ++n) issue_next(g * S + n);
@@ -419,11 +449,12 @@ static int dc_launch(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
   return check_launch("k_sus_dc");
 }
 
-// Fields handled here: q = 16 (check degree <= 4, variable degree <= 3); the
-// environment variable GFQ_SUS_DC_MINQ (4 or 8) extends it to smaller fields
-// (measurement: the transform kernel has no layout switches there either).
+// Fields handled here: q = 8 and 16 (check degree <= 4, variable degree <= 3).
+// The environment variable GFQ_SUS_DC_MINQ moves the lower end (4, 8, 16):
+// measured on C3 (q = 8, 4096 frames) 3.47 -> 3.81 TB/s model against the
+// transform kernel, on C2 (q = 4) 1.80 -> 1.74 (profiles/r02/dc_small_fields.txt).
 #ifndef GFQ_SUS_DC_MINQ_DEFAULT
-#define GFQ_SUS_DC_MINQ_DEFAULT 16
+#define GFQ_SUS_DC_MINQ_DEFAULT 8
 #endif
 bool sus_dc_applies(const WaveArgs &a) {
   static int minq = -1;
