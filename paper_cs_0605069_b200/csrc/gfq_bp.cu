@@ -864,7 +864,7 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
         for (int gg = 0; gg < G; ++gg)
           if (gg == g) su[gg] = s;
         return done;
-      });
+      }, lvl_begin);
     }
     return;
   }
@@ -877,7 +877,8 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
   float *rsm = (float *)(scr + SS::XR_D * 8);
   int m = 0;  // ping-pong transpose counter
   long long lo, hi;
-  group_range(ntask, (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
+  sus_group_range(a, lvl_begin, ncols, (long long)(*a.nactive), (long long)blockIdx.x * G + g,
+                  (long long)gridDim.x * G, lo, hi);
   // producer cursor over (task, unit) of this group
   UnitWalker pc;
   if (producer) pc.init(a, lo, hi, ncols, lvl_begin);

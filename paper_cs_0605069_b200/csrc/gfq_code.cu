@@ -105,7 +105,7 @@ using namespace gfq;
 
 extern "C" const char *gfq_last_error(void) { return g_err.c_str(); }
 
-extern "C" int gfq_version(void) { return 0x010000; }
+extern "C" int gfq_version(void) { return 0x010100; }  // 1.1: params.compaction, p = 8, GFQ_NKERNELS 15
 
 extern "C" int gfq_code_create(gfq_code **out, int p, unsigned poly, int N, int M,
                                long long nnzA, const int *A_row, const int *A_col,

@@ -283,6 +283,37 @@ __device__ __forceinline__ void group_range(long long ntask, long long gg, long 
   if (lo > ntask) lo = ntask;
 }
 
+// SUS: the share of global group gg of the (frame block, column) tasks of one
+// level, balanced by UNITS (a column of degree dv is dv units of work: source
+// columns have 3, noise columns 2, and a level lists its source columns first,
+// so a split by columns gave some groups 1.5x the work of others -- 12 % of the
+// warp slots of k_sus_dc idle at C4, profiles/r02).  Boundaries stay at column
+// starts: lo / hi = the first task whose first unit is at or after the group's
+// share of the nblk * U unit positions (U = units of the level).
+__device__ __forceinline__ long long sus_task_at(const LvlCol *lc, int ncols, int U, int u_first, long long nblk,
+                                                 long long p) {
+  if (p >= nblk * U) return nblk * ncols;
+  const long long fbi = p / U;
+  const int r = (int)(p - fbi * U);
+  int lo = 0, hi = ncols;   // first column whose unit offset is >= r
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (lc[mid].unit0 - u_first >= r) hi = mid; else lo = mid + 1;
+  }
+  return fbi * ncols + lo;
+}
+__device__ __forceinline__ void sus_group_range(const WaveArgs &a, int lvl_begin, int ncols, long long nblk,
+                                                long long gg, long long ngroups, long long &lo, long long &hi) {
+  const LvlCol *lc = a.c.lvl_col + lvl_begin;
+  const int u_first = lc[0].unit0;
+  const LvlCol last = lc[ncols - 1];
+  const int U = last.unit0 + (last.dv > 0 ? last.dv : 1) - u_first;
+  const long long total = nblk * U;
+  const long long chunk = (total + ngroups - 1) / ngroups;
+  lo = sus_task_at(lc, ncols, U, u_first, nblk, gg * chunk);
+  hi = sus_task_at(lc, ncols, U, u_first, nblk, (gg + 1) * chunk);
+}
+
 // Stage header written by the producer (plain shared store, published by the
 // mbarrier arrive) followed by TMA-fetched metadata:
 //   [0,64) TaskInfo  [128,256) CheckDesc | SusDesc(128..192) + VarDesc(192..256)
@@ -813,14 +844,17 @@ struct Cursor {
 // complete (SUS tasks span several stages).
 template <int S, int G, typename Issue>
 __device__ __forceinline__ void produce(const WaveArgs &a, uint64_t *bars, long long ntask, int nitems,
-                                        Issue issue) {
+                                        Issue issue, int sus_lvl_begin = -1) {
   const long long ngroups = (long long)gridDim.x * G;
   Cursor cur[G];
   int ring[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     long long lo, hi;
-    group_range(ntask, (long long)blockIdx.x * G + g, ngroups, lo, hi);
+    if (sus_lvl_begin >= 0)
+      sus_group_range(a, sus_lvl_begin, nitems, ntask / nitems, (long long)blockIdx.x * G + g, ngroups, lo, hi);
+    else
+      group_range(ntask, (long long)blockIdx.x * G + g, ngroups, lo, hi);
     cur[g].init(a, lo, hi, nitems);
     ring[g] = 0;
   }

@@ -99,8 +99,12 @@ __device__ __forceinline__ void dc_issue(const WaveArgs &a, int fb, const LvlUni
 // unit is being processed (a second UnitWalker running one unit ahead, whose
 // record was itself prefetched a step earlier): the later TMA load is an L2 hit.
 // In flight: 148 SMs x 15 warps x <= 6 KB, far below the 126 MB of L2.
-#ifndef GFQ_DC_L2_PREFETCH
-#define GFQ_DC_L2_PREFETCH 1
+// Measured (profiles/r02/dc_variants.txt): C4 (q = 16, 6 KB units) 3.30 -> 3.36
+// TB/s model; C3 (q = 8, 3 KB units) 3.80 -> 3.11: the producer lane's extra
+// work outweighs the shorter wait there, so it is on from q = 16 only.  Two
+// stages x 10 warps instead: C4 2.49, C3 3.37 TB/s.
+#ifndef GFQ_DC_L2_PREFETCH_MINQ
+#define GFQ_DC_L2_PREFETCH_MINQ 16
 #endif
 template <int Q>
 __device__ __forceinline__ void dc_prefetch_unit(const WaveArgs &a, int fb, const LvlUnit &un) {
@@ -341,11 +345,12 @@ __global__ void __launch_bounds__(DCShape<Q, DMAX, DVMAX, MARKOV, S, W>::THREADS
   float *rsm = (float *)(sp.scr + (size_t)g * DS::RSM);
   const bool producer = (lane == 0);
   long long lo, hi;
-  group_range(ntask, (long long)blockIdx.x * W + g, (long long)gridDim.x * W, lo, hi);
+  sus_group_range(a, lvl_begin, ncols, (long long)(*a.nactive), (long long)blockIdx.x * W + g,
+                  (long long)gridDim.x * W, lo, hi);
   UnitWalker pc, la;   // la runs S units ahead of pc (L2 prefetch)
   if (producer) {
     pc.init(a, lo, hi, ncols, lvl_begin);
-    if (GFQ_DC_L2_PREFETCH) {
+    if (Q >= GFQ_DC_L2_PREFETCH_MINQ) {
       la.init(a, lo, hi, ncols, lvl_begin);
       for (int n = 0; n < S && la.valid(); ++n) (void)la.take(a);
     }
@@ -356,7 +361,7 @@ __global__ void __launch_bounds__(DCShape<Q, DMAX, DVMAX, MARKOV, S, W>::THREADS
     const LvlUnit un = pc.take(a);
     dc_issue<Q, MARKOV>(a, fb, un, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA,
                         sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k);
-    if (GFQ_DC_L2_PREFETCH && la.valid()) {
+    if (Q >= GFQ_DC_L2_PREFETCH_MINQ && la.valid()) {
       const int fb1 = la.fb;
       const LvlUnit un1 = la.take(a);   // an L1 hit: prefetched when la took the unit before it
       dc_prefetch_unit<Q>(a, fb1, un1);

@@ -13,18 +13,22 @@
 // instruction), and nothing crosses a warp except the intermediate product of
 // a degree-4 check (8 KB through the consumed input slot).
 //
-// Decomposition: a group of 2 warps owns a unit for its 32 frames (one frame
-// per lane); warp c computes the 32 outputs y = 32c .. 32c+31 (16 FFMA2
-// accumulator pairs, kept twice: even and odd x contribute to the pair in
-// natural and swapped order).  The operand B of a convolution lives in the
-// registers of both warps (32 pairs, stored XOR-shifted by 16c so that every
-// register index of the unrolled loop is a compile-time constant); the operand
-// A streams from shared memory, one value per lane per x.
+// Decomposition: a group of 4 warps owns a unit for its 32 frames (one frame
+// per lane); warp c computes the 16 outputs y = 16c .. 16c+15.  With x = 16 xh
+// + xl the XOR-convolution splits into 16 x 16 block convolutions:
+//   S[16c + yl] = sum_xh sum_xl A[16 xh + xl] * B[16 (c ^ xh) + (yl ^ xl)],
+// so the kernel loops over xh = 0..3 (run time) around ONE unrolled block
+// convolution (128 FFMA2: the 8 accumulator pairs are kept twice, even and odd
+// xl contribute to a pair in natural and swapped order) whose operands -- A
+// block xh and B block c ^ xh, 16 values each -- are loaded from the stage by
+// address, so every register index is a compile-time constant and the code
+// stays a few KB (the first version, fully unrolled over all 64 x, spent 41 %
+// of its cycles on instruction-cache misses: profiles/r02/dc64).
 //   u_k(y) = q_ij_k(h_k^-1 y)             (rows chosen at load)
-//   S(y)   = sum_x A(x) B(y ^ x)          (64 x 32 FFMA per warp = 1024 FFMA2 per thread)
+//   S(y)   = sum_x A(x) B(y ^ x)          (4 x 128 FFMA2 per thread and convolution)
 //   r_ij(a) = S(z_i ^ h_ij a)             (Eq. 3; reading A4)
 // The variable update (Eq. 4, posterior Eq. 5, clipping) is in fp64 as in the
-// other kernels, streamed over the entries, 32 per warp, two passes.
+// other kernels, streamed over the entries, 16 per warp, two passes.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -42,7 +46,7 @@ namespace gfq {
 #define GFQ_DC64_S 1   // TMA stages per group
 #endif
 
-constexpr int DQ = 64, DPB = 6, DW = 2;   // field size, bits, warps per group
+constexpr int DQ = 64, DW = 4;   // field size, warps per group
 
 template <int S, int G>
 struct DC64Shape {
@@ -71,59 +75,56 @@ __device__ __forceinline__ void lds_v4(uint32_t addr, uint32_t (&w)[4]) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(addr) : "memory");
 }
 
-// B operand of this warp: Bc[i] = (B[2(i ^ 16c)], B[2(i ^ 16c) + 1]) from a
-// message slot, rows h^-1 y (rt_row: shared address of rowtab[h^-1][0]).
-__device__ __forceinline__ void dc64_load_B(uint32_t slot_lane, uint32_t rt_row, int c, u64 (&Bc)[32]) {
+// 16 values of a message from a stage slot: entries y0 .. y0+15 (y0 a multiple
+// of 16).  PERM: rows h^-1 y through the offset table (rt_row: shared address
+// of rowtab[h^-1][0]); else natural rows.
+template <bool PERM>
+__device__ __forceinline__ void dc64_load16(uint32_t slot_lane, uint32_t rt_row, int y0, float (&v)[16]) {
+  if constexpr (PERM) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    uint32_t w[4];
-    lds_v4(rt_row + (uint32_t)(((4 * j) ^ (16 * c)) * 4), w);   // offsets of y = 2i, 2i+1 for i = (4j ^ 16c) .. +3
+    for (int j = 0; j < 2; ++j) {
+      uint32_t w[4];
+      lds_v4(rt_row + (uint32_t)(y0 * 2 + j * 16), w);
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const float lo = lds_f32(slot_lane + (w[t] & 0xffffu));
-      const float hi = lds_f32(slot_lane + (w[t] >> 16));
-      Bc[4 * j + t] = pack2(lo, hi);
+      for (int t = 0; t < 4; ++t) {
+        v[8 * j + 2 * t] = lds_f32(slot_lane + (w[t] & 0xffffu));
+        v[8 * j + 2 * t + 1] = lds_f32(slot_lane + (w[t] >> 16));
+      }
     }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = lds_f32(slot_lane + (uint32_t)((y0 + k) * 128));
   }
 }
 
-// The same from a natural-order fp32 vector (the intermediate product t).
-__device__ __forceinline__ void dc64_load_B_nat(uint32_t slot_lane, int c, u64 (&Bc)[32]) {
+// S(y) = sum_x A(x) B(y ^ x) for this warp's 16 outputs y = 16c + yl.
+template <bool APERM, bool BPERM>
+__device__ __forceinline__ void dc64_conv(uint32_t a_lane, uint32_t a_rt, uint32_t b_lane, uint32_t b_rt, int c,
+                                          float (&s)[16]) {
+  u64 an[8], as_[8];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const uint32_t y0 = (uint32_t)(2 * (i ^ (16 * c)));
-    Bc[i] = pack2(lds_f32(slot_lane + y0 * 128), lds_f32(slot_lane + (y0 + 1) * 128));
-  }
-}
-
-// S(y) = sum_x A(x) B(y ^ x) for this warp's 32 outputs y = 32c + 2 ml + {0, 1}.
-// A streams from shared memory (APERM: rows h^-1 x through the offset table,
-// else natural rows).
-template <bool APERM>
-__device__ __forceinline__ void dc64_conv(uint32_t a_lane, uint32_t rt_row, const u64 (&Bc)[32], float (&s)[32]) {
-  u64 an[16], as_[16];
+  for (int ml = 0; ml < 8; ++ml) { an[ml] = 0ull; as_[ml] = 0ull; }
+#pragma unroll 1
+  for (int xh = 0; xh < 4; ++xh) {
+    float av[16], bv[16];
+    dc64_load16<APERM>(a_lane, a_rt, 16 * xh, av);
+    dc64_load16<BPERM>(b_lane, b_rt, 16 * (c ^ xh), bv);
+    u64 Bb[8];
 #pragma unroll
-  for (int ml = 0; ml < 16; ++ml) { an[ml] = 0ull; as_[ml] = 0ull; }
+    for (int i = 0; i < 8; ++i) Bb[i] = pack2(bv[2 * i], bv[2 * i + 1]);
 #pragma unroll
-  for (int xb = 0; xb < 8; ++xb) {
-    uint32_t w[4] = {0u, 0u, 0u, 0u};
-    if constexpr (APERM) lds_v4(rt_row + (uint32_t)(xb * 16), w);
+    for (int xl = 0; xl < 16; ++xl) {
+      const u64 axx = pack2(av[xl], av[xl]);
 #pragma unroll
-    for (int xi = 0; xi < 8; ++xi) {
-      const int x = xb * 8 + xi;
-      const uint32_t off = APERM ? ((xi & 1) ? (w[xi >> 1] >> 16) : (w[xi >> 1] & 0xffffu)) : (uint32_t)(x * 128);
-      const float ax = lds_f32(a_lane + off);
-      const u64 axx = pack2(ax, ax);
-#pragma unroll
-      for (int ml = 0; ml < 16; ++ml) {
-        // output pair m = 16c + ml reads B pair m ^ (x >> 1) = Bc[ml ^ (x >> 1)]
-        if (x & 1) fma2(as_[ml], axx, Bc[ml ^ (x >> 1)]);
-        else fma2(an[ml], axx, Bc[ml ^ (x >> 1)]);
+      for (int ml = 0; ml < 8; ++ml) {
+        // output pair ml of the block reads B pair ml ^ (xl >> 1)
+        if (xl & 1) fma2(as_[ml], axx, Bb[ml ^ (xl >> 1)]);
+        else fma2(an[ml], axx, Bb[ml ^ (xl >> 1)]);
       }
     }
   }
 #pragma unroll
-  for (int ml = 0; ml < 16; ++ml) {
+  for (int ml = 0; ml < 8; ++ml) {
     float n0, n1, s0, s1;
     unpack2(an[ml], n0, n1);
     unpack2(as_[ml], s0, s1);   // odd x: (B[2m'+1], B[2m']) feed (s[2m], s[2m+1])
@@ -142,42 +143,29 @@ __device__ __forceinline__ void dc64_check(const WaveArgs &a, const unsigned cha
   const SusDesc *sd = (const SusDesc *)(hdr + 128);
   const int z = hdr[256 + lane];
   const unsigned long long pke = sd->perm_e;
-  float S[32];
+  float S[16];
   if constexpr (DO == 0) {
     if (release) release_stage(empty, lane);
 #pragma unroll
-    for (int k = 0; k < 32; ++k) S[k] = (c == 0 && k == 0) ? 1.0f : 0.0f;   // the point mass at 0
+    for (int k = 0; k < 16; ++k) S[k] = (c == 0 && k == 0) ? 1.0f : 0.0f;   // the point mass at 0
   } else if constexpr (DO == 1) {
-    uint32_t w[4];
-    const uint32_t rt_row = rt + (uint32_t)((sd->perm_o[0] & 0xff) * DQ * 2);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      lds_v4(rt_row + (uint32_t)(c * 64 + j * 16), w);
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        S[8 * j + 2 * t] = lds_f32(pay_lane + (w[t] & 0xffffu));
-        S[8 * j + 2 * t + 1] = lds_f32(pay_lane + (w[t] >> 16));
-      }
-    }
+    dc64_load16<true>(pay_lane, rt + (uint32_t)((sd->perm_o[0] & 0xff) * DQ * 2), 16 * c, S);
     if (release) release_stage(empty, lane);
   } else {
-    // DO = 2 or 3 (run-time: one copy of each convolution body in the kernel)
-    u64 Bc[32];
+    // DO = 2 or 3 (run time: one copy of each convolution body in the kernel)
     const uint32_t rt0 = rt + (uint32_t)((sd->perm_o[0] & 0xff) * DQ * 2);
     const uint32_t rt1 = rt + (uint32_t)((sd->perm_o[1] & 0xff) * DQ * 2);
-    dc64_load_B(pay_lane, rt0, c, Bc);                       // B = message 0
-    dc64_conv<true>(pay_lane + DQ * 128, rt1, Bc, S);        // A = message 1
+    dc64_conv<true, true>(pay_lane + DQ * 128, rt1, pay_lane, rt0, c, S);   // A = message 1, B = message 0
     if (ti.d - 1 >= 3) {
-      // the intermediate product goes to slot 0 (message 0 is in the registers of
-      // both warps): both must be done with it before either overwrites it
+      // the intermediate product goes to slot 0: every warp of the group must
+      // be done reading message 0 before any of them overwrites it
       group_bar<DW>(g);
 #pragma unroll
-      for (int k = 0; k < 32; ++k)
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(pay_lane + (uint32_t)((32 * c + k) * 128)), "f"(S[k]) : "memory");
+      for (int k = 0; k < 16; ++k)
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(pay_lane + (uint32_t)((16 * c + k) * 128)), "f"(S[k]) : "memory");
       const uint32_t rt2 = rt + (uint32_t)((sd->perm_o[2] & 0xff) * DQ * 2);
-      dc64_load_B(pay_lane + 2 * DQ * 128, rt2, c, Bc);      // B = message 2
-      group_bar<DW>(g);                                      // the product is complete
-      dc64_conv<false>(pay_lane, 0u, Bc, S);                 // A = the product (natural order)
+      group_bar<DW>(g);                                                     // the product is complete
+      dc64_conv<false, true>(pay_lane, 0u, pay_lane + 2 * DQ * 128, rt2, c, S);   // A = the product, B = message 2
     }
     if (release) release_stage(empty, lane);
   }
@@ -190,9 +178,9 @@ __device__ __forceinline__ void dc64_check(const WaveArgs &a, const unsigned cha
                           ? (unsigned char *)(a.rmsg + ((size_t)ti.fb * a.c.E + ti.e0 + ti.s) * DQ * 32 + lane)
                           : nullptr;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
+  for (int j = 0; j < 2; ++j) {
     uint32_t w[4];
-    lds_v4(rte + (uint32_t)(c * 64 + j * 16), w);
+    lds_v4(rte + (uint32_t)(c * 32 + j * 16), w);
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const uint32_t o0 = (w[t] & 0xffffu) ^ hz, o1 = (w[t] >> 16) ^ hz;
@@ -207,8 +195,8 @@ __device__ __forceinline__ void dc64_check(const WaveArgs &a, const unsigned cha
   }
 }
 
-// SUS step 2 (+ step 4, reading A8) for the column by the group's two warps:
-// warp c takes entries 32c .. 32c+31 (chunks of 8 for the prior).
+// SUS step 2 (+ step 4, reading A8) for the column by the group's four warps:
+// warp c takes entries 16c .. 16c+15 (two chunks of 8 for the prior).
 template <int DV>
 __device__ __forceinline__ void dc64_vn(const WaveArgs &a, const unsigned char *hdr, const unsigned char *xtra,
                                         const float *rsm, double *red, int g, int c, int lane, bool frozen) {
@@ -237,13 +225,13 @@ __device__ __forceinline__ void dc64_vn(const WaveArgs &a, const unsigned char *
 #pragma unroll
   for (int t = 0; t < NS; ++t) sums[t] = 0.0;
 #pragma unroll 1
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < 2; ++u) {
     double pr[8];
-    prior_from<DQ, 8, false>(a, j, 4 * c + u, lane, (const float *)xtra, nullptr, pr);
+    prior_from<DQ, 8, false>(a, j, 2 * c + u, lane, (const float *)xtra, nullptr, pr);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       double o[NS];
-      prods(pr[k], (4 * c + u) * 8 + k, o);
+      prods(pr[k], (2 * c + u) * 8 + k, o);
 #pragma unroll
       for (int t = 0; t < NS; ++t) sums[t] += o[t];
       mx = fmax(mx, o[DV]);
@@ -254,8 +242,15 @@ __device__ __forceinline__ void dc64_vn(const WaveArgs &a, const unsigned char *
   red[(NS * DW + c) * 32 + lane] = mx;
   group_bar<DW>(g);
 #pragma unroll
-  for (int t = 0; t < NS; ++t) sums[t] = red[(t * DW) * 32 + lane] + red[(t * DW + 1) * 32 + lane];
-  mx = fmax(red[(NS * DW) * 32 + lane], red[(NS * DW + 1) * 32 + lane]);
+  for (int t = 0; t < NS; ++t) {
+    double v = red[(t * DW) * 32 + lane];
+#pragma unroll
+    for (int cc = 1; cc < DW; ++cc) v += red[(t * DW + cc) * 32 + lane];
+    sums[t] = v;
+  }
+  mx = red[(NS * DW) * 32 + lane];
+#pragma unroll
+  for (int cc = 1; cc < DW; ++cc) mx = fmax(mx, red[(NS * DW + cc) * 32 + lane]);
   int bad = 0;
   double inv[NS];
   float add[NS];
@@ -274,12 +269,12 @@ __device__ __forceinline__ void dc64_vn(const WaveArgs &a, const unsigned char *
   for (int t = 0; t < DV; ++t) qrow[t] = a.qmsg + ((size_t)fb * E + vd->qdst[t]) * DQ * 32 + lane;
   float *qarow = a.qall ? a.qall + ((size_t)fb * a.c.V + j) * DQ * 32 + lane : nullptr;
 #pragma unroll 1
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < 2; ++u) {
     double pr[8];
-    prior_from<DQ, 8, false>(a, j, 4 * c + u, lane, (const float *)xtra, nullptr, pr);
+    prior_from<DQ, 8, false>(a, j, 2 * c + u, lane, (const float *)xtra, nullptr, pr);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int y = (4 * c + u) * 8 + k;
+      const int y = (2 * c + u) * 8 + k;
       double o[NS];
       prods(pr[k], y, o);
       if (o[DV] >= thr && bidx == DQ) bidx = y;
@@ -294,7 +289,8 @@ __device__ __forceinline__ void dc64_vn(const WaveArgs &a, const unsigned char *
   ired[c * 32 + lane] = bidx;
   group_bar<DW>(g);
   if (c == 0) {
-    bidx = min(bidx, ired[32 + lane]);
+#pragma unroll
+    for (int cc = 1; cc < DW; ++cc) bidx = min(bidx, ired[cc * 32 + lane]);
     if (bidx >= DQ || !okq) bidx = 0;
     if (!frozen) {
       a.xhat[((size_t)fb * a.c.V + j) * 32 + lane] = (unsigned char)bidx;
@@ -322,7 +318,8 @@ __global__ void __launch_bounds__(DC64Shape<S, G>::THREADS) k_sus_dc64(WaveArgs 
   float *rsm = (float *)(sp.scr + (size_t)g * DS::RSM);
   const bool producer = (c == 0) && (lane == 0);
   long long lo, hi;
-  group_range(ntask, (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
+  sus_group_range(a, lvl_begin, ncols, (long long)(*a.nactive), (long long)blockIdx.x * G + g,
+                  (long long)gridDim.x * G, lo, hi);
   UnitWalker pc;
   if (producer) pc.init(a, lo, hi, ncols, lvl_begin);
   auto issue_next = [&](int k) {
