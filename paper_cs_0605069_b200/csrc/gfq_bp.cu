@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
         vn_issue<Q, DVMAX, MARKOV>(a, cu.fb, cu.item, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA,
                                    sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k, clip_only);
         return true;
-      });
+      }, -1, !clip_only);
     return;
   }
   const int cw = PW ? warp - 1 : warp;
@@ -412,7 +412,8 @@ __global__ void __launch_bounds__(VNShape<Q, KR, DVMAX, MARKOV, S, G>::THREADS)
   const bool producer = !PW && (c == 0) && (lane == 0);
   double *red = (double *)(sp.scr + (size_t)g * VS::SCR);
   long long lo, hi;
-  group_range(ntask, (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
+  if (clip_only) group_range(ntask, (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
+  else vn_group_range(a, (long long)(*a.nactive), (long long)blockIdx.x * G + g, (long long)gridDim.x * G, lo, hi);
   Cursor pc;
   if (producer) {
     pc.init(a, lo, hi, V);

@@ -283,6 +283,8 @@ __device__ __forceinline__ void group_range(long long ntask, long long gg, long 
   if (lo > ntask) lo = ntask;
 }
 
+constexpr long long kBalanceMinTasks = 1 << 16;   // below this a launch is too short to pay for the searches
+
 // SUS: the share of global group gg of the (frame block, column) tasks of one
 // level, balanced by UNITS (a column of degree dv is dv units of work: source
 // columns have 3, noise columns 2, and a level lists its source columns first,
@@ -304,6 +306,12 @@ __device__ __forceinline__ long long sus_task_at(const LvlCol *lc, int ncols, in
 }
 __device__ __forceinline__ void sus_group_range(const WaveArgs &a, int lvl_begin, int ncols, long long nblk,
                                                 long long gg, long long ngroups, long long &lo, long long &hi) {
+  // small launches: the binary searches (dependent L2 loads) would cost more
+  // than the imbalance; the plain split by columns is exact enough
+  if (nblk * ncols < kBalanceMinTasks) {
+    group_range(nblk * ncols, gg, ngroups, lo, hi);
+    return;
+  }
   const LvlCol *lc = a.c.lvl_col + lvl_begin;
   const int u_first = lc[0].unit0;
   const LvlCol last = lc[ncols - 1];
@@ -312,6 +320,39 @@ __device__ __forceinline__ void sus_group_range(const WaveArgs &a, int lvl_begin
   const long long chunk = (total + ngroups - 1) / ngroups;
   lo = sus_task_at(lc, ncols, U, u_first, nblk, gg * chunk);
   hi = sus_task_at(lc, ncols, U, u_first, nblk, (gg + 1) * chunk);
+}
+
+// PUS variable node: the same balancing by work for the (block, variable)
+// tasks -- a variable of degree dv moves 2 dv q-vectors, and the source
+// variables (degree 3, plus the Markov prior) come before the noise variables
+// (degree 2).  Weight of variable j: dv_j + 1 (+ 2 for a Markov source
+// variable's two neighbour rows); its offset is col_ptr[j] + j (+ 2 min(j, N)).
+__device__ __forceinline__ long long vn_weight_off(const WaveArgs &a, int j) {
+  return (long long)__ldg(a.c.col_ptr + j) + j + (a.markov ? 2 * (j < a.c.N ? j : a.c.N) : 0);
+}
+__device__ __forceinline__ long long vn_task_at(const WaveArgs &a, long long Wt, long long nblk, long long p) {
+  const int V = a.c.V;
+  if (p >= nblk * Wt) return nblk * V;
+  const long long fbi = p / Wt;
+  const long long r = p - fbi * Wt;
+  int lo = 0, hi = V;   // first variable whose weight offset is >= r
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (vn_weight_off(a, mid) >= r) hi = mid; else lo = mid + 1;
+  }
+  return fbi * V + lo;
+}
+__device__ __forceinline__ void vn_group_range(const WaveArgs &a, long long nblk, long long gg, long long ngroups,
+                                               long long &lo, long long &hi) {
+  if (nblk * a.c.V < kBalanceMinTasks) {
+    group_range(nblk * a.c.V, gg, ngroups, lo, hi);
+    return;
+  }
+  const long long Wt = a.c.E + a.c.V + (a.markov ? 2LL * a.c.N : 0);
+  const long long total = nblk * Wt;
+  const long long chunk = (total + ngroups - 1) / ngroups;
+  lo = vn_task_at(a, Wt, nblk, gg * chunk);
+  hi = vn_task_at(a, Wt, nblk, (gg + 1) * chunk);
 }
 
 // Stage header written by the producer (plain shared store, published by the
@@ -844,7 +885,7 @@ struct Cursor {
 // complete (SUS tasks span several stages).
 template <int S, int G, typename Issue>
 __device__ __forceinline__ void produce(const WaveArgs &a, uint64_t *bars, long long ntask, int nitems,
-                                        Issue issue, int sus_lvl_begin = -1) {
+                                        Issue issue, int sus_lvl_begin = -1, bool vn_weighted = false) {
   const long long ngroups = (long long)gridDim.x * G;
   Cursor cur[G];
   int ring[G];
@@ -853,6 +894,8 @@ __device__ __forceinline__ void produce(const WaveArgs &a, uint64_t *bars, long 
     long long lo, hi;
     if (sus_lvl_begin >= 0)
       sus_group_range(a, sus_lvl_begin, nitems, ntask / nitems, (long long)blockIdx.x * G + g, ngroups, lo, hi);
+    else if (vn_weighted)
+      vn_group_range(a, ntask / nitems, (long long)blockIdx.x * G + g, ngroups, lo, hi);
     else
       group_range(ntask, (long long)blockIdx.x * G + g, ngroups, lo, hi);
     cur[g].init(a, lo, hi, nitems);

@@ -35,7 +35,10 @@ namespace gfq {
 
 // warps per CTA / stages per warp (tuning knobs)
 #ifndef GFQ_DC_W
-#define GFQ_DC_W 15
+#define GFQ_DC_W 16      // q = 16: 16 warps x 108 registers, 216 KB (measured 15 -> 16: C4 3.58 -> 3.78 TB/s)
+#endif
+#ifndef GFQ_DC_W_SMALL
+#define GFQ_DC_W_SMALL 32  // q <= 8: 64 registers per thread, 7 KB per warp
 #endif
 #ifndef GFQ_DC_S
 #define GFQ_DC_S 1
@@ -434,7 +437,7 @@ constexpr int dc_warps(int want) {
 
 template <int Q, bool MK>
 static int dc_launch(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
-  constexpr int S = MK ? GFQ_DC_S_MARKOV : GFQ_DC_S, W = dc_warps<Q, MK, S>(GFQ_DC_W);
+  constexpr int S = MK ? GFQ_DC_S_MARKOV : GFQ_DC_S, W = dc_warps<Q, MK, S>(Q >= 16 ? GFQ_DC_W : GFQ_DC_W_SMALL);
   using DS = DCShape<Q, 4, 3, MK, S, W>;
   static_assert(DS::SMEM <= 232448, "k_sus_dc: shared memory");
   auto k = k_sus_dc<Q, 4, 3, MK, S, W>;
