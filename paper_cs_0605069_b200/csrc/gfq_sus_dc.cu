@@ -37,6 +37,9 @@ namespace gfq {
 #ifndef GFQ_DC_W
 #define GFQ_DC_W 16      // q = 16: 16 warps x 108 registers, 216 KB (measured 15 -> 16: C4 3.58 -> 3.78 TB/s)
 #endif
+#ifndef GFQ_DC_VN_UNROLL
+#define GFQ_DC_VN_UNROLL 2   // entries of the streamed variable node in flight
+#endif
 #ifndef GFQ_DC_W_SMALL
 #define GFQ_DC_W_SMALL 32  // q <= 8: 64 registers per thread, 7 KB per warp
 #endif
@@ -49,6 +52,8 @@ namespace gfq {
 #ifndef GFQ_DC_FFMA2
 #define GFQ_DC_FFMA2 1
 #endif
+
+constexpr int kDcVnUnroll = GFQ_DC_VN_UNROLL;
 
 template <int Q, int DMAX, int DVMAX, bool MARKOV, int S, int W>
 struct DCShape {
@@ -275,7 +280,7 @@ __device__ __forceinline__ void dc_vn(const WaveArgs &a, const unsigned char *hd
   double sums[NS], mx = 0.0;
 #pragma unroll
   for (int t = 0; t < NS; ++t) sums[t] = 0.0;
-#pragma unroll 2
+#pragma unroll kDcVnUnroll
   for (int k = 0; k < Q; ++k) {
     double o[NS];
     prods(k, o);
@@ -301,7 +306,7 @@ __device__ __forceinline__ void dc_vn(const WaveArgs &a, const unsigned char *hd
   for (int t = 0; t < DV; ++t) qrow[t] = a.qmsg + ((size_t)fb * E + vd->qdst[t]) * Q * 32 + lane;
   float *qsrow = (a.markov && j < a.c.N && a.qs_new) ? a.qs_new + ((size_t)fb * a.c.N + j) * Q * 32 + lane : nullptr;
   float *qarow = a.qall ? a.qall + ((size_t)fb * a.c.V + j) * Q * 32 + lane : nullptr;
-#pragma unroll 2
+#pragma unroll kDcVnUnroll
   for (int k = 0; k < Q; ++k) {
     double o[NS];
     prods(k, o);
