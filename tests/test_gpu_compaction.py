@@ -108,3 +108,39 @@ def test_bad_compaction_value_is_rejected(gfq):
     prm = gfq.Params(gfq.GFQ_BSC, fr.ch_param, 0, 5, compaction=7)
     with pytest.raises(gfq.GfqError):
         gfq.gfq_decode(gcode, torch.as_tensor(fr.obs).cuda(), prm)
+
+
+def test_compaction_with_sus_orders_and_host_entry(gfq):
+    """Caller-supplied SUS orders (A35) and the host-buffer entry with frame compaction."""
+    cfg = synth.CONFIGS["C3"]
+    code = synth.code_for(cfg)
+    fr = synth.frames_for(cfg, code, range(150), point=3)
+    gcode = gfq.Code.from_synth(code)
+    rng = np.random.default_rng(35)
+    orders = np.stack([rng.permutation(code.N + code.M) for _ in range(3)]).astype(np.int32)
+    res = {}
+    for comp in (gfq.GFQ_COMPACT_BLOCKS, gfq.GFQ_COMPACT_FRAMES):
+        prm = gfq.Params(gfq.GFQ_BIAWGN, fr.ch_param, 1, 80, early_exit=True, sus_order=orders, compaction=comp)
+        s_hat, it, ws = gfq.gfq_decode(gcode, torch.as_tensor(fr.obs).cuda(), prm)
+        ph = gfq.Params(gfq.GFQ_BIAWGN, fr.ch_param, 0, 80, early_exit=True, compaction=comp)
+        sh, ih, _ = gfq.gfq_decode_host(gcode, torch.as_tensor(fr.obs), ph)
+        res[comp] = (s_hat.cpu().numpy(), it.cpu().numpy(), sh.numpy().copy(), ih.numpy().copy())
+    for a, b in zip(res[gfq.GFQ_COMPACT_BLOCKS], res[gfq.GFQ_COMPACT_FRAMES]):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("nframes", [1, 31, 33, 65])
+def test_compaction_small_and_ragged_batches(gfq, nframes):
+    cfg = synth.CONFIGS["C1"]
+    code = synth.code_for(cfg)
+    fr = synth.frames_for(cfg, code, range(nframes))
+    gcode = gfq.Code.from_synth(code)
+    outs = []
+    for comp in (gfq.GFQ_COMPACT_BLOCKS, gfq.GFQ_COMPACT_FRAMES):
+        for sched in (0, 1):
+            prm = gfq.Params(gfq.GFQ_BSC, fr.ch_param, sched, 100, early_exit=True, compaction=comp)
+            s_hat, it, ws = gfq.gfq_decode(gcode, torch.as_tensor(fr.obs).cuda(), prm)
+            outs.append((comp, sched, s_hat.cpu().numpy(), it.cpu().numpy()))
+    for sched in (0, 1):
+        a = [o for o in outs if o[1] == sched]
+        assert np.array_equal(a[0][2], a[1][2]) and np.array_equal(a[0][3], a[1][3])
