@@ -78,9 +78,12 @@ constexpr int fit_stages(size_t per_stage, size_t other, int max_s) {
 #ifndef GFQ_PW_T4
 #define GFQ_PW_T4 1
 #endif
+#ifndef GFQ_PW_T8
+#define GFQ_PW_T8 0
+#endif
 template <int T>
 struct PWof {
-  static constexpr bool v = ((T == 2 && GFQ_PW_T2) || (T == 4 && GFQ_PW_T4));  // measured: in-group producers win for T = 1, 8
+  static constexpr bool v = ((T == 2 && GFQ_PW_T2) || (T == 4 && GFQ_PW_T4) || (T == 8 && GFQ_PW_T8));  // measured: in-group producers win for T = 1, 8
 };
 #ifndef GFQ_G_T8_CN
 #define GFQ_G_T8_CN 2
