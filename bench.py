@@ -208,8 +208,8 @@ def run_reference(args, cfg, iters, F):
     return 0
 
 
-ARITH = {8: "q*r fp32 direct convolution (SUS), fp64 transforms (PUS), fp64 variable node; fp32 storage",
-         16: "q*r fp32 direct convolution (SUS), fp64 transforms (PUS), fp64 variable node; fp32 storage",
+ARITH = {8: "check node: fp32 direct XOR-convolution (PUS and SUS); variable node fp64; fp32 storage",
+         16: "check node: fp32 direct XOR-convolution (PUS and SUS); variable node fp64; fp32 storage",
          64: "fp64 registers (transforms, products, normalisation), fp32 message storage"}
 
 

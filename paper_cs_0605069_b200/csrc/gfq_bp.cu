@@ -1120,6 +1120,7 @@ static int sus_q(const WaveArgs &a, int lb, int ncols, cudaStream_t s) {
 
 int launch_cn(const WaveArgs &a, cudaStream_t s) {
   if (big_applies(a)) return launch_big_cn(a, s);
+  if (cn_dc_applies(a)) return launch_cn_dc(a, s);
 #define F(Q) cn_q<Q>(a, s)
   GFQ_DISPATCH_Q(a.c.q, F)
 #undef F

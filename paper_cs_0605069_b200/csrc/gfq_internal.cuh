@@ -176,6 +176,8 @@ int launch_vn(const WaveArgs &a, cudaStream_t s);
 int launch_sus_level(const WaveArgs &a, int level, int ncols, cudaStream_t s);
 bool sus_dc_applies(const WaveArgs &a);   // gfq_sus_dc.cu
 int launch_sus_dc(const WaveArgs &a, int level, int ncols, cudaStream_t s);
+bool cn_dc_applies(const WaveArgs &a);    // gfq_sus_dc.cu: PUS check node by direct convolution (q = 8, 16)
+int launch_cn_dc(const WaveArgs &a, cudaStream_t s);
 bool sus_dc64_applies(const WaveArgs &a); // gfq_sus_dc64.cu: q = 64 by direct convolution
 int launch_sus_dc64(const WaveArgs &a, int level, int ncols, cudaStream_t s);
 bool big_applies(const WaveArgs &a);      // gfq_bigq.cu: q = 256

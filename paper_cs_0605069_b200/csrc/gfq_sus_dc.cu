@@ -430,6 +430,204 @@ __global__ void __launch_bounds__(DCShape<Q, DMAX, DVMAX, MARKOV, S, W>::THREADS
   }
 }
 
+// ============================================================== PUS check node by direct convolution
+// The horizontal pass (Eq. 3) for q <= 16 with the same arithmetic
+// as the SUS unit above: one warp owns a check for its 32 frames; for every
+// edge k it convolves the permuted messages of the other edges (fp32 FFMA2,
+// non-negative terms) and writes q * r_k.  The syndrome shift r_k(a) =
+// S(z ^ h_k a) is folded into the load of the first other message,
+// u'(y) = u(y ^ z) (a per-lane XOR of the shared-memory row: rows are 128-byte
+// lines of 32 lanes, so it is bank-conflict free), which makes the output rows
+// uniform over the lanes: every store is one coalesced 128-byte line.
+// Why: k_cn at q = 16 holds a whole check in fp64 registers (254 per thread,
+// 8 warps per SM) and stalls on instruction fetch (72 KB of straight-line code,
+// profiles/r02/c4_pus_details.csv); this kernel is short, fp32 and runs 16+
+// warps per SM.  A degree-4 check costs 8 convolutions here against 6 with
+// prefix / suffix products: the multiply-adds are not what limits it.
+template <int Q, int DMAX, int S, int W>
+struct CNDCShape {
+  static constexpr size_t PAY = (size_t)DMAX * Q * 128;
+  static constexpr size_t TSM_B = (size_t)2 * Q * Q;   // row-offset table
+  using Sh = Shape<Q, S, W, PAY, 0, 0, TSM_B, false>;
+  static constexpr size_t SMEM = Sh::SMEM;
+  static constexpr int THREADS = W * 32;
+};
+
+template <int Q>
+__device__ __forceinline__ void cndc_issue(const WaveArgs &a, int fb, int i, unsigned char *hdr, unsigned char *pay,
+                                           uint64_t *full) {
+  const int e0 = __ldg(a.c.row_ptr + i), d = __ldg(a.c.row_ptr + i + 1) - e0;
+  TaskInfo *ti = (TaskInfo *)hdr;
+  ti->fb = fb; ti->item = i; ti->e0 = e0; ti->deg = d;
+  const uint32_t msg = (uint32_t)d * Q * 128;
+  mbar_expect_tx(full, 128 + 32 + (a.early_exit ? 128 : 0) + msg);
+  bulk_g2s(hdr + 128, a.c.check_desc + i, 128, full);
+  bulk_g2s(hdr + 256, a.z + ((size_t)fb * a.c.M + i) * 32, 32, full);
+  if (a.early_exit) bulk_g2s(hdr + 384, a.conv + fb * 32, 128, full);
+  if (msg) bulk_g2s(pay, a.qmsg + ((size_t)fb * a.c.E + e0) * Q * 32, msg, full);
+}
+
+// u[y] = message(h^-1 (y ^ z)): dc_load with the per-lane syndrome shift hz = (h^-1 z) << 7
+template <int Q>
+__device__ __forceinline__ void dc_load_shift(uint32_t slot_lane, uint32_t rt, unsigned long long pk, uint32_t hz,
+                                              float (&u)[Q]) {
+  uint32_t ad[Q];
+  tab_addrs_sm<Q, Q>(0u, rt, pk, 0, ad);
+#pragma unroll
+  for (int y = 0; y < Q; ++y) u[y] = lds_f32(slot_lane + (ad[y] ^ hz));
+}
+
+template <int Q, int D>
+__device__ __forceinline__ void cndc_check(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_lane, uint32_t rt,
+                                           int lane, bool frozen) {
+  const TaskInfo ti = *(const TaskInfo *)hdr;
+  const CheckDesc *cd = (const CheckDesc *)(hdr + 128);
+  const int z = hdr[256 + lane];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    float S[Q];
+    if constexpr (D == 1) {
+      // no other edge: the point mass at 0 shifted by z, S'(y) = [y = z]
+#pragma unroll
+      for (int y = 0; y < Q; ++y) S[y] = (y == z) ? 1.0f : 0.0f;
+    } else {
+      // the other edges in row order; the first of them carries the shift
+      constexpr int NO = D - 1;
+      int o[NO];
+#pragma unroll
+      for (int t = 0, x = 0; t < D; ++t)
+        if (t != k) o[x++] = t;
+      const unsigned long long pk0 = cd->perm[o[0]];
+      uint32_t hz;
+      asm volatile("ld.shared.u16 %0, [%1];" : "=r"(hz) : "r"(rt + (uint32_t)(((pk0 & 0xff) * Q + z) * 2)));
+      if constexpr (NO == 1) {
+        dc_load_shift<Q>(pay_lane + (uint32_t)(o[0] * Q * 128), rt, pk0, hz, S);
+      } else {
+        float u[Q], v[Q];
+        dc_load_shift<Q>(pay_lane + (uint32_t)(o[0] * Q * 128), rt, pk0, hz, u);
+        dc_load<Q>(pay_lane + (uint32_t)(o[1] * Q * 128), rt, cd->perm[o[1]], v);
+        if constexpr (NO == 2) {
+          dc_conv<Q>(u, v, S);
+        } else {
+          static_assert(NO == 3, "cndc_check: check degree <= 4");
+          float w[Q], t2[Q];
+          dc_load<Q>(pay_lane + (uint32_t)(o[2] * Q * 128), rt, cd->perm[o[2]], w);
+          dc_conv<Q>(u, v, t2);
+          dc_conv<Q>(t2, w, S);
+        }
+      }
+    }
+    // r_k(a) = S'(h_k a): S'[y] goes to row a = h_k^-1 y of the edge's canonical slot
+    if (!frozen) {
+      uint32_t ad[Q];
+      tab_addrs_sm<Q, Q>(0u, rt, cd->perm[k], 0, ad);
+      unsigned char *dst = (unsigned char *)(a.rmsg + ((size_t)ti.fb * a.c.E + cd->canon[k]) * Q * 32 + lane);
+#pragma unroll
+      for (int y = 0; y < Q; ++y) *(float *)(dst + ad[y]) = S[y] * (float)Q;
+    }
+  }
+}
+
+template <int Q, int S, int W>
+__global__ void __launch_bounds__(CNDCShape<Q, 4, S, W>::THREADS) k_cn_dc(WaveArgs a) {
+  using CS = CNDCShape<Q, 4, S, W>;
+  using Sh = typename CS::Sh;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const SmemPtrs sp = smem_ptrs<Sh, S, W>(smem);
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  if (threadIdx.x == 0) init_bars<S, W>(sp.bars, 1);
+  unsigned short *rtab = (unsigned short *)sp.tsm;
+  for (int k = threadIdx.x; k < Q * Q; k += blockDim.x) rtab[k] = a.c.rowtab[k];
+  const uint32_t rt = smem_u32(rtab);
+  __syncthreads();
+  const int M = a.c.M;
+  const long long ntask = (long long)(*a.nactive) * M;
+  const bool producer = (lane == 0);
+  long long lo, hi;
+  group_range(ntask, (long long)blockIdx.x * W + g, (long long)gridDim.x * W, lo, hi);
+  Cursor pc;
+  if (producer) {
+    pc.init(a, lo, hi, M);
+    for (int n = 0; n < S && pc.valid(); ++n) {
+      const int k = g * S + n;
+      cndc_issue<Q>(a, pc.fb, pc.item, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA, sp.bars + k);
+      pc.advance(a);
+    }
+  }
+  for (long long task = lo; task < hi; ++task) {
+    const int rr = (int)(task - lo), st = rr % S, k = g * S + st;
+    const unsigned char *hdr = sp.hdr + (size_t)k * kHdr;
+    const uint32_t pay_lane = sp.pay_u32 + (uint32_t)((size_t)k * Sh::PAYA) + lane * 4;
+    uint64_t *empty = sp.bars + W * S + k;
+    const uint32_t par = (uint32_t)((rr / S) & 1);
+    mbar_wait(sp.bars + k, par);
+    const int d = ((const TaskInfo *)hdr)->deg;
+    const bool frozen = a.early_exit && ((const int *)(hdr + 384))[lane] != 0;
+    switch (d) {
+      case 0: break;
+      case 1: cndc_check<Q, 1>(a, hdr, pay_lane, rt, lane, frozen); break;
+      case 2: cndc_check<Q, 2>(a, hdr, pay_lane, rt, lane, frozen); break;
+      case 3: cndc_check<Q, 3>(a, hdr, pay_lane, rt, lane, frozen); break;
+      default: cndc_check<Q, 4>(a, hdr, pay_lane, rt, lane, frozen); break;
+    }
+    release_stage(empty, lane);
+    if (producer && pc.valid()) {
+      mbar_wait(empty, par);
+      cndc_issue<Q>(a, pc.fb, pc.item, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA, sp.bars + k);
+      pc.advance(a);
+    }
+  }
+}
+
+// measured (profiles/r02/dc_variants.txt): q = 16: 2 stages x 12 warps 10.03 ms per C4 launch
+// (1 x 16: 11.07, 3 x 8: 12.95; k_cn: 12.00); q = 8: 1 x 16 1.267 ms per C3 launch (2 x 16: 1.328; k_cn: 1.383)
+#ifndef GFQ_CNDC_W
+#define GFQ_CNDC_W 12     // q = 16: warps per CTA / stages per warp (8 KB per stage)
+#endif
+#ifndef GFQ_CNDC_S
+#define GFQ_CNDC_S 2
+#endif
+#ifndef GFQ_CNDC_W8
+#define GFQ_CNDC_W8 16    // q = 8 (4 KB per stage)
+#endif
+#ifndef GFQ_CNDC_S8
+#define GFQ_CNDC_S8 1
+#endif
+template <int Q>
+static int cndc_launch(const WaveArgs &a, cudaStream_t s) {
+  constexpr int S = Q >= 16 ? GFQ_CNDC_S : GFQ_CNDC_S8, W = Q >= 16 ? GFQ_CNDC_W : GFQ_CNDC_W8;
+  using CS = CNDCShape<Q, 4, S, W>;
+  static_assert(CS::SMEM <= 232448, "k_cn_dc: shared memory");
+  auto k = k_cn_dc<Q, S, W>;
+  const int grid = grid_for(k, CS::THREADS, CS::SMEM, ((long long)a.nfb * a.c.M + W - 1) / W);
+  k<<<grid, CS::THREADS, CS::SMEM, s>>>(a);
+  return check_launch("k_cn_dc");
+}
+
+// q = 8, 16 with check degree <= 4; GFQ_CN_DC=0 / 1 in the environment overrides
+// the build-time default.
+#ifndef GFQ_CN_DC_DEFAULT
+#define GFQ_CN_DC_DEFAULT 1
+#endif
+bool cn_dc_applies(const WaveArgs &a) {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("GFQ_CN_DC");
+    on = e ? (atoi(e) != 0) : GFQ_CN_DC_DEFAULT;
+  }
+  return on && (a.c.q == 8 || a.c.q == 16) && a.c.max_cdeg <= 4;
+}
+
+int launch_cn_dc(const WaveArgs &a, cudaStream_t s) {
+  switch (a.c.q) {
+    case 8: return cndc_launch<8>(a, s);
+    case 16: return cndc_launch<16>(a, s);
+    default: break;
+  }
+  set_error("k_cn_dc: unsupported q");
+  return GFQ_EUNSUPPORTED;
+}
+
 // most warps per CTA (<= want) whose stages fit the 227 KB of shared memory
 template <int Q, bool MK, int S>
 constexpr int dc_warps(int want) {

@@ -25,3 +25,18 @@ def test_dc64_variant_passes_the_c5_sus_gates():
                        env=env, capture_output=True, text=True, timeout=1500, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "2 passed" in r.stdout, r.stdout[-2000:]
+
+
+def test_transform_check_node_stays_covered_at_q16_and_q8():
+    """PUS at q = 8, 16 runs the direct-convolution check node k_cn_dc by default;
+    GFQ_CN_DC=0 selects the transform kernel k_cn (still used for check degree
+    > 4): its C3 / C4 PUS message gates run here in a subprocess."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, GFQ_CN_DC="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-q", "-x",
+                        "-p", "no:cacheprovider", "-k", "(C3 or C4) and PUS and message_gate"],
+                       env=env, capture_output=True, text=True, timeout=1500, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "3 passed" in r.stdout, r.stdout[-2000:]
