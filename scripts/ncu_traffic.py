@@ -15,7 +15,8 @@ for rep in reps:
         d = dict(zip(hdr, vals))
         u = dict(zip(hdr, un))
         name = d["Kernel Name"].split("<")[0].split("(")[0].replace("void ", "").replace("gfq::", "")
-        short = {"k_cn": "cn", "k_vn": "vn", "k_sus": "sus", "k_sus_dc": "sus"}.get(name, name)
+        short = {"k_cn": "cn", "k_cn_dc": "cn", "k_big_cn": "cn", "k_vn": "vn", "k_big_vn": "vn", "k_sus": "sus",
+                 "k_sus_dc": "sus", "k_sus_dc64": "sus", "k_big_sus": "sus"}.get(name, name)
         def num(k):
             try:
                 return float(d[k])
