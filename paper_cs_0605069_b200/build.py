@@ -16,7 +16,8 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(HERE, "..", "include", "gfq.h")]
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh"))]
+    deps.append(os.path.join(HERE, "..", "include", "gfq.h"))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
@@ -83,6 +84,46 @@ def build_sync_check(force: bool = False) -> str:
         return obj
     with ThreadPoolExecutor(max_workers=len(KERNEL_SOURCES)) as ex:
         objs = list(ex.map(one, KERNEL_SOURCES))
+    objs += [os.path.join(CSRC, f.replace(".cu", ".o")) for f in SOURCES if f not in KERNEL_SOURCES]
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", SYNC_CHECK_LIB, *objs,
+           "-Xcompiler", "-fPIC"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("link failed:\n%s" % res.stderr[-8000:])
+    return SYNC_CHECK_LIB
+
+
+def build_all(force: bool = False):
+    """libgfq.so and libgfq_synccheck.so with their compiles running side by side
+    (gfq_bp.cu alone takes minutes; the two variants of it are independent)."""
+    from concurrent.futures import ThreadPoolExecutor
+    srcs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh"))]
+    srcs.append(os.path.join(HERE, "..", "include", "gfq.h"))
+    newest = max(os.path.getmtime(d) for d in srcs)
+    sync_fresh = os.path.exists(SYNC_CHECK_LIB) and os.path.getmtime(SYNC_CHECK_LIB) > newest
+    if not force and sync_fresh:
+        build()
+        return SYNC_CHECK_LIB
+    # compile the sync-check objects of the kernel sources while build() compiles the default ones
+    def sync_objs():
+        out = []
+        for src in KERNEL_SOURCES:
+            obj = os.path.join(CSRC, src.replace(".cu", "_synccheck.o"))
+            cmd = [NVCC, *FLAGS, "-DGFQ_SYNC_CHECK=1", "-c", os.path.join(CSRC, src), "-o", obj]
+            out.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+        return out
+    procs = sync_objs()
+    with ThreadPoolExecutor(max_workers=1) as ex:
+        fut = ex.submit(build, force)
+        errs = []
+        for src, pr in zip(KERNEL_SOURCES, procs):
+            _, err = pr.communicate()
+            if pr.returncode != 0:
+                errs.append("nvcc failed for %s (sync check):\n%s" % (src, err[-8000:]))
+        fut.result()
+    if errs:
+        raise RuntimeError(errs[0])
+    objs = [os.path.join(CSRC, f.replace(".cu", "_synccheck.o")) for f in KERNEL_SOURCES]
     objs += [os.path.join(CSRC, f.replace(".cu", ".o")) for f in SOURCES if f not in KERNEL_SOURCES]
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", SYNC_CHECK_LIB, *objs,
            "-Xcompiler", "-fPIC"]
