@@ -416,7 +416,8 @@ def _low_degree_code(p, N, M, seed):
     return rows, cols, vals, A, B
 
 
-@pytest.mark.parametrize("p,markov", [(4, False), (4, True), (5, False), (6, False), (6, True)])
+@pytest.mark.parametrize("p,markov", [(3, False), (3, True), (4, False), (4, True), (5, False), (6, False), (6, True),
+                                      (8, False)])
 def test_low_degree_code_large_field_message_parity(gfq, p, markov):
     N, M = 30, 50
     for seed in range(300, 400):
