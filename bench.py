@@ -398,8 +398,8 @@ def decode_run(args, cfg, F, iters, schedules, steps, warmup, gfq, shard, dist, 
     # ---------------- CPU oracle baseline (rank 0, N=1 only): ~10-30 s of the box's cores
     if not args.no_cpu and rank == 0 and world == 1:
         ncores = os.cpu_count() or 1
-        si = 2
-        sf = max(1, min(2 * ncores, 64))
+        si = 3
+        sf = max(1, min(4 * ncores, 128))      # ~10-20 s of the host's cores at C5
         sample = argparse.Namespace(channel=cfg.channel, ch_param=param, obs=obs_host[:sf].numpy())
         dt, thr = oracle_sample_rate(cfg, code, sample, sf, si, [0 if s == gfq.GFQ_PUS else 1 for s in schedules])
         t_full = dt * iters / si
