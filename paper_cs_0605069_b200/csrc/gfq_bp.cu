@@ -583,6 +583,23 @@ __device__ __forceinline__ void row_addrs(uint32_t base, uint32_t rt, const unsi
   if constexpr (RTS) tab_addrs_sm<Q, KR>(base, rt, pk, c, ad);
   else tab_addrs<Q, KR>(base, rowtab, pk, c, ad);
 }
+// The same with the rows shifted by the syndrome: entry y reads row h^-1 (y ^ z)
+// = h^-1 y ^ h^-1 z (multiplication by h^-1 is GF(2)-linear); z differs per
+// lane, the XOR acts on the row bits only, and a lane still reads its own
+// 4-byte column of a 128-byte row: no bank conflict.  Shifting ONE operand of
+// the convolution shifts the result, S'(y) = S(y ^ z), so r(a) = S(z ^ h a) =
+// S'(h a) needs no sign (-1)^{w.z} in the transform domain (reading A4).
+template <int Q, int KR, bool RTS>
+__device__ __forceinline__ void row_addrs_shift(uint32_t base, uint32_t rt, const unsigned short *rowtab,
+                                                unsigned long long pk, int c, int z, uint32_t (&ad)[KR]) {
+  uint32_t off[KR];
+  row_addrs<Q, KR, RTS>(0u, rt, rowtab, pk, c, off);
+  uint32_t hz;
+  if constexpr (RTS) asm volatile("ld.shared.u16 %0, [%1];" : "=r"(hz) : "r"(rt + (uint32_t)(((pk & 0xff) * Q + z) * 2)));
+  else hz = rowtab[(size_t)(pk & 0xff) * Q + z];
+#pragma unroll
+  for (int k = 0; k < KR; ++k) ad[k] = base + (off[k] ^ hz);
+}
 
 template <int Q, int KR, int DO, bool RTS, typename RF>
 __device__ __forceinline__ void sus_check_phased(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_u32,
@@ -622,7 +639,10 @@ __device__ __forceinline__ void sus_check_phased(const WaveArgs &a, const unsign
 #pragma unroll
     for (int t = 0; t < DO; ++t) {
       uint32_t ad[KR];
-      row_addrs<Q, KR, RTS>(pay_u32 + (uint32_t)(t * Q * 128 + lane * 4), rt, rowtab, sd->perm_o[t], c, ad);
+      if (t == 0)   // the first other message carries the syndrome shift
+        row_addrs_shift<Q, KR, RTS>(pay_u32 + (uint32_t)(lane * 4), rt, rowtab, sd->perm_o[0], c, z, ad);
+      else
+        row_addrs<Q, KR, RTS>(pay_u32 + (uint32_t)(t * Q * 128 + lane * 4), rt, rowtab, sd->perm_o[t], c, ad);
 #pragma unroll
       for (int k = 0; k < KR; ++k) v[t][k] = (double)lds_f32(ad[k]);
     }
@@ -654,14 +674,12 @@ __device__ __forceinline__ void sus_check_phased(const WaveArgs &a, const unsign
     }
 #pragma unroll
     for (int t = 0; t < DO; ++t) wht_bits<KR, LKR - LT, LKR>(v[t]);
-    uint32_t sm[KR];
-    sign_masks<KR, T>(z, c, sm);
 #pragma unroll
     for (int k = 0; k < KR; ++k) {
       double x = v[0][k];
 #pragma unroll
       for (int t = 1; t < DO; ++t) x *= v[t][k];
-      acc[k] = flip(x, sm[k]);
+      acc[k] = x;
     }
     wht_bits<KR, LKR - LT, LKR>(acc);
     elided_bar<T>(g);  // the inverse switch overwrites the buffer just read
