@@ -315,10 +315,19 @@ def decode_run(args, cfg, F, iters, schedules, steps, warmup, gfq, shard, dist, 
                             frac=achieved / peak, traffic=traffic, alg_bytes_per_launch=alg / k_n,
                             launches=k_n, avg_launch_ms=k_ms / k_n, traffic_source=tsrc, peak_source=peak_src)
     dom = max(roofs, key=lambda k: kinds[k][0]) if roofs else None
+    # per schedule: the hot kernels of one schedule together (PUS = cn + vn, SUS = the level kernel)
+    per_sched = {}
+    for sname, ks in (("pus", ("cn", "vn")), ("sus", ("sus",))):
+        if all(k in roofs for k in ks):
+            t_ms = sum(kinds[k][0] for k in ks)
+            alg = 16.0 * cfg.q * cfg.E * F * iters          # 2E updates x 8q bytes per frame-iteration
+            per_sched[sname] = dict(kernel_ms_per_step=t_ms, ms_per_iteration=t_ms / iters,
+                                    achieved=alg / (t_ms / 1e3) / 1e9, peak=peak, unit="GB/s",
+                                    frac=alg / (t_ms / 1e3) / 1e9 / peak)
     model_gbs = model_bytes_per_frame_iter(cfg) * F * iters * len(schedules) * steps / (ms / 1e3) / 1e9
     out = dict(value=value, ms_per_step=ms / steps, ms_per_step_instrumented=ms_prof,
                edge_msg_updates_per_s=edge_updates / (ms / 1e3), model_hbm_gbs=model_gbs,
-               roofline=roofs.get(dom), rooflines=roofs, clocks=clk,
+               roofline=roofs.get(dom), rooflines=roofs, schedule_rooflines=per_sched, clocks=clk,
                gpu_launches=int(launches_per_step * steps),
                kernels={k: dict(ms=v[0], launches=v[1]) for k, v in kinds.items()},
                health=dict(zero_normalisers_last_decode=st["zero_normalisers"]),
@@ -456,7 +465,8 @@ def main():
             config=head["config"],
             edge_msg_updates_per_s=head["edge_msg_updates_per_s"], model_hbm_gbs=head["model_hbm_gbs"],
             ms_per_step_instrumented=head["ms_per_step_instrumented"],
-            roofline=head["roofline"], rooflines=head["rooflines"], cpu_baseline=head.get("cpu_baseline"),
+            roofline=head["roofline"], rooflines=head["rooflines"], schedule_rooflines=head["schedule_rooflines"],
+            cpu_baseline=head.get("cpu_baseline"),
             e2e=head.get("e2e"), clocks=head["clocks"], gpu_launches=head["gpu_launches"],
             kernels=head["kernels"], health=head["health"], convergence=head.get("convergence"),
             secondary=sec,
