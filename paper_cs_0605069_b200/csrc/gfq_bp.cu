@@ -504,13 +504,12 @@ struct SUSShape {
 // CURRENT q's of the check's other edges (the transform of k_cn restricted to
 // one output).  Writes q * r_ij into rsm slot s in natural order a.
 template <int Q, int KR, int DO, int DMAX, typename RF>
-__device__ __forceinline__ void sus_check(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_u32,
+__device__ __forceinline__ void sus_check(const WaveArgs &a, const TaskInfo &ti, const unsigned char *hdr, uint32_t pay_u32,
                                           uint64_t *empty, bool release, double *xp, int &m, float *rsm, int g,
                                           int c, int lane, bool frozen, RF &&refill) {
   using C = QC<Q, KR>;
   constexpr int T = C::T, LKR = C::LKR, LT = C::LT, P = C::P;
   constexpr bool PP = PPof<Q>::v;
-  const TaskInfo ti = *(const TaskInfo *)hdr;
   const SusDesc *sd = (const SusDesc *)(hdr + 128);
   const int z = hdr[256 + lane];
   double v[DO > 0 ? DO : 1][KR];
@@ -602,14 +601,13 @@ __device__ __forceinline__ void row_addrs_shift(uint32_t base, uint32_t rt, cons
 }
 
 template <int Q, int KR, int DO, bool RTS, typename RF>
-__device__ __forceinline__ void sus_check_phased(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_u32,
+__device__ __forceinline__ void sus_check_phased(const WaveArgs &a, const TaskInfo &ti, const unsigned char *hdr, uint32_t pay_u32,
                                                  double *stage_x, uint64_t *empty, bool last, double *xp,
                                                  float *rsm, uint32_t rt, const unsigned short *rowtab,
                                                  int g, int c, int lane, bool frozen, RF &&refill) {
   using C = QC<Q, KR>;
   constexpr int T = C::T, LKR = C::LKR, LT = C::LT;
   static_assert(T > 1 && DO <= 3, "phased SUS check: q >= 16, degree <= 4");
-  const TaskInfo ti = *(const TaskInfo *)hdr;
   const SusDesc *sd = (const SusDesc *)(hdr + 128);
   const int z = hdr[256 + lane];
   const unsigned long long pke = sd->perm_e;
@@ -734,7 +732,7 @@ __device__ __forceinline__ void wht_bits_f(float (&u)[KR]) {
 }
 
 template <int Q, int KR, int DO, bool RTS, typename RF>
-__device__ __forceinline__ void sus_check_fwd32(const WaveArgs &a, const unsigned char *hdr, uint32_t pay_u32,
+__device__ __forceinline__ void sus_check_fwd32(const WaveArgs &a, const TaskInfo &ti, const unsigned char *hdr, uint32_t pay_u32,
                                                 double *stage_x, uint64_t *empty, bool last, double *xp,
                                                 float *rsm, uint32_t rt, const unsigned short *rowtab,
                                                 int g, int c, int lane, bool frozen, RF &&refill) {
@@ -742,7 +740,6 @@ __device__ __forceinline__ void sus_check_fwd32(const WaveArgs &a, const unsigne
   constexpr int T = C::T, LKR = C::LKR, LT = C::LT;
   static_assert(T > 1 && DO >= 1 && DO <= 3, "fwd32 SUS check: q >= 16, 2 <= degree <= 4");
   static_assert((size_t)3 * Q * 32 * 4 <= (size_t)2 * Q * 32 * 8, "three fp32 messages fit the scratch");
-  const TaskInfo ti = *(const TaskInfo *)hdr;
   const SusDesc *sd = (const SusDesc *)(hdr + 128);
   const int z = hdr[256 + lane];
   const unsigned long long pke = sd->perm_e;
@@ -805,10 +802,9 @@ __device__ __forceinline__ void sus_check_fwd32(const WaveArgs &a, const unsigne
 }
 
 template <int Q, int KR, int DV, int DVMAX, bool MARKOV, bool ONEBAR, typename RF>
-__device__ __forceinline__ void sus_vn(const WaveArgs &a, const unsigned char *hdr, const unsigned char *xtra,
+__device__ __forceinline__ void sus_vn(const WaveArgs &a, const TaskInfo &ti, const unsigned char *hdr, const unsigned char *xtra,
                                        const float *Tsm, uint64_t *empty, const float *rsm, double *red, int g,
                                        int c, int lane, bool frozen, bool late_release, RF &&refill) {
-  const TaskInfo ti = *(const TaskInfo *)hdr;
   const VarDesc *vd = (const VarDesc *)(hdr + 192);
   int qdst[DV > 0 ? DV : 1];
   double r[DV > 0 ? DV : 1][KR];
@@ -828,6 +824,65 @@ __device__ __forceinline__ void sus_vn(const WaveArgs &a, const unsigned char *h
   if (late_release) {  // red lives in the stage payload
     release_stage(empty, lane);
     refill();
+  }
+}
+
+// ---------------------------------------------------------------- distributed stage issue (8-warp groups)
+// With one producer lane per group, warp 0 of an 8-warp group executed ~25 %
+// more instructions than the other seven (the unit walk, the header stores and
+// 5-7 TMA issues per unit), and the group barriers made everybody wait for it:
+// the read after the first barrier of a unit held 22 % of k_sus's stall samples
+// at C5 (profiles/r02).  Here every warp of the group walks the units itself
+// (UnitWalker, warp-uniform) and its lane 0 issues one share of the copies:
+//   warp 0: the unit record (LvlUnit, 32 B -> header) and payload run 0
+//   warp 1: payload run 1          warp 2: SusDesc and the syndrome row
+//   warp 3: frame-state row, VarDesc (last unit)     warp 4: the prior's extra rows
+// Warp 0 posts the stage's expect_tx for the unit that will REFILL a stage just
+// before its own arrival on the stage's "empty" barrier; the other warps issue
+// only after that barrier's phase has completed (which needs warp 0's
+// arrival), so every complete_tx follows the expect_tx.  Nobody writes the
+// header with plain stores any more: the consumers take the unit's fields from
+// the TMA-copied record and the frame block from their own walker.
+// MEASURED (profiles/r02/dc_variants.txt): correct (106 GPU tests) but 2.7 %
+// SLOWER at C5 (182.6 vs 177.8 ms per sweep): seven more unit walks and five
+// more waits per unit cost more than warp 0's detour saves -- the wait at the
+// first barrier is the warp scheduler's, not the producer's.  Off by default.
+#ifndef GFQ_SUS_DIST_ISSUE
+#define GFQ_SUS_DIST_ISSUE 0
+#endif
+template <int Q, bool MARKOV>
+__device__ __forceinline__ uint32_t sus_unit_tx_bytes(const WaveArgs &a, const LvlUnit &un) {
+  const int nunits = un.dv > 0 ? un.dv : 1;
+  const bool last = (un.s == nunits - 1);
+  uint32_t b = 32;                                           // the unit record
+  if (un.dv > 0) b += 64 + 32 + (uint32_t)(un.d - 1) * Q * 128;   // SusDesc, z row, the d-1 other messages
+  if (a.early_exit) b += 128;
+  if (last) b += 64 + extras_bytes<Q, MARKOV>(a, un.j);
+  return b;
+}
+template <int Q, bool MARKOV>
+__device__ __forceinline__ void sus_issue_share(const WaveArgs &a, int fb, int u, const LvlUnit &un, unsigned char *hdr,
+                                                unsigned char *pay, unsigned char *xtra, uint64_t *full, int c) {
+  const int nunits = un.dv > 0 ? un.dv : 1;
+  const bool last = (un.s == nunits - 1);
+  const float *rowbase = a.qmsg + ((size_t)fb * a.c.E + un.r0) * Q * 32;
+  if (c == 0) {
+    bulk_g2s(hdr, a.c.lvl_unit + u, 32, full);
+    if (un.dv > 0 && un.pos > 0) bulk_g2s(pay, rowbase, (uint32_t)un.pos * Q * 128, full);
+  } else if (c == 1) {
+    if (un.dv > 0 && un.d - 1 - un.pos > 0)
+      bulk_g2s(pay + (size_t)un.pos * Q * 128, rowbase + (size_t)(un.pos + 1) * Q * 32,
+               (uint32_t)(un.d - 1 - un.pos) * Q * 128, full);
+  } else if (c == 2) {
+    if (un.dv > 0) {
+      bulk_g2s(hdr + 128, a.c.sus_desc + un.e0 + un.s, 64, full);
+      bulk_g2s(hdr + 256, a.z + ((size_t)fb * a.c.M + un.i) * 32, 32, full);
+    }
+  } else if (c == 3) {
+    if (a.early_exit) bulk_g2s(hdr + 384, a.conv + fb * 32, 128, full);
+    if (last) bulk_g2s(hdr + 192, a.c.var_desc + un.j, 64, full);
+  } else if (c == 4) {
+    if (last) issue_extras<Q, MARKOV>(a, fb, un.j, xtra, full);
   }
 }
 
@@ -899,8 +954,9 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
   sus_group_range(a, lvl_begin, ncols, (long long)(*a.nactive), (long long)blockIdx.x * G + g,
                   (long long)gridDim.x * G, lo, hi);
   // producer cursor over (task, unit) of this group
+  constexpr bool DIST = (T == 8) && !PW && (GFQ_SUS_DIST_ISSUE != 0) && (S <= 2);
   UnitWalker pc;
-  if (producer) pc.init(a, lo, hi, ncols, lvl_begin);
+  if (producer || DIST) pc.init(a, lo, hi, ncols, lvl_begin);
   auto issue_next = [&](int k) {
     if (!pc.valid()) return;
     const int fb = pc.fb;
@@ -908,8 +964,44 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
     sus_issue_rec<Q, MARKOV>(a, fb, un, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA,
                              sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k);
   };
-  if (producer)
-    for (int n = 0; n < S; ++n) issue_next(g * S + n);
+  // DIST: the unit each stage will be refilled with (taken when the stage's
+  // current unit is released) and the frame blocks of the units in flight
+  int fbq0 = 0, fbq1 = 0;        // frame block of the unit in stage 0 / 1 of this group
+  LvlUnit nxt_un;                // the unit taken at the last release (valid if nxt_ok)
+  int nxt_fb = 0, nxt_u = 0;
+  bool nxt_ok = false;
+  auto dist_take = [&]() {       // every warp, warp-uniform
+    nxt_ok = pc.valid();
+    if (nxt_ok) {
+      nxt_fb = pc.fb;
+      nxt_u = pc.u;
+      nxt_un = pc.take(a);
+    }
+  };
+  auto dist_expect = [&](int k) {   // warp 0's lane 0, before its arrival on empty[k]
+    if (nxt_ok && c == 0 && lane == 0)
+      mbar_expect_tx(sp.bars + k, sus_unit_tx_bytes<Q, MARKOV>(a, nxt_un));
+  };
+  auto dist_issue = [&](int k, int st) {   // after the stage's empty phase (or in the prologue)
+    if (!nxt_ok) return;
+    if (st == 0) fbq0 = nxt_fb; else fbq1 = nxt_fb;
+    if (lane == 0 && c <= 4)
+      sus_issue_share<Q, MARKOV>(a, nxt_fb, nxt_u, nxt_un, sp.hdr + (size_t)k * kHdr, sp.pay + (size_t)k * Sh::PAYA,
+                                 sp.xtra + (size_t)k * Sh::XTRA_A, sp.bars + k, c);
+  };
+  if constexpr (DIST) {
+    // prologue: expect_tx of the first S units by warp 0, a group barrier, then the shares
+#pragma unroll
+    for (int n = 0; n < S; ++n) {
+      dist_take();
+      dist_expect(g * S + n);
+      group_bar<T>(g);
+      dist_issue(g * S + n, n);
+    }
+  } else {
+    if (producer)
+      for (int n = 0; n < S; ++n) issue_next(g * S + n);
+  }
   int rr = 0;  // units consumed by this group
   for (long long task = lo; task < hi; ++task) {
     int nunits = 1;
@@ -921,13 +1013,36 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       const uint32_t pay_u32 = sp.pay_u32 + (uint32_t)((size_t)k * Sh::PAYA);
       uint64_t *empty = sp.bars + G * S + k;
       auto refill = [&]() {
-        if (producer && pc.valid()) {
-          mbar_wait(empty, (uint32_t)((rr / S) & 1));
-          issue_next(k);
+        if constexpr (DIST) {
+          // (release_stage ran just before: warp 0 posted the next expect_tx in it, see below)
+          if (nxt_ok) {
+            if (lane == 0 && c <= 4) mbar_wait(empty, (uint32_t)((rr / S) & 1));
+            dist_issue(k, st);
+          }
+        } else {
+          if (producer && pc.valid()) {
+            mbar_wait(empty, (uint32_t)((rr / S) & 1));
+            issue_next(k);
+          }
         }
       };
       mbar_wait(sp.bars + k, (uint32_t)((rr / S) & 1));
-      const TaskInfo *ti = (const TaskInfo *)hdr;
+      TaskInfo tinfo;
+      if constexpr (DIST) {
+        const LvlUnit lu = *(const LvlUnit *)hdr;
+        tinfo.fb = (st == 0) ? fbq0 : fbq1;
+        tinfo.item = lu.j; tinfo.e0 = lu.e0; tinfo.deg = lu.dv;
+        tinfo.s = lu.s; tinfo.r0 = lu.r0; tinfo.d = lu.d; tinfo.pos = lu.pos; tinfo.i = lu.i;
+        // the unit that will refill this stage: taken now, its expect_tx posted by
+        // warp 0 right here -- before ANY warp of the group can release the stage
+        // (every release follows this point in program order, and the other warps'
+        // copies follow the completion of the empty phase, which needs warp 0's release)
+        dist_take();
+        dist_expect(k);
+      } else {
+        tinfo = *(const TaskInfo *)hdr;
+      }
+      const TaskInfo *ti = &tinfo;
       const int dv = ti->deg, d = ti->d;
       nunits = dv > 0 ? dv : 1;
       const bool last = (s == nunits - 1);
@@ -935,8 +1050,8 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       double *stage_x = (double *)(sp.pay + (size_t)k * Sh::PAYA);
       if constexpr (SS::PHASED) {
         if (dv > 0) {
-#define SP(n) sus_check_phased<Q, KR, n, SS::RTS>(a, hdr, pay_u32, stage_x, empty, last, xp, rsm, rt, a.c.rowtab, g, c, lane, frozen, refill)
-#define SP32(n) sus_check_fwd32<Q, KR, n, SS::RTS>(a, hdr, pay_u32, stage_x, empty, last, xp, rsm, rt, a.c.rowtab, g, c, lane, frozen, refill)
+#define SP(n) sus_check_phased<Q, KR, n, SS::RTS>(a, tinfo, hdr, pay_u32, stage_x, empty, last, xp, rsm, rt, a.c.rowtab, g, c, lane, frozen, refill)
+#define SP32(n) sus_check_fwd32<Q, KR, n, SS::RTS>(a, tinfo, hdr, pay_u32, stage_x, empty, last, xp, rsm, rt, a.c.rowtab, g, c, lane, frozen, refill)
           if constexpr (GFQ_SUS_FWD32 != 0) {
             switch (d - 1) {
               case 0: SP(0); break;
@@ -956,7 +1071,7 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
 #undef SP32
         }
       } else if (dv > 0) {
-#define SC(n) sus_check<Q, KR, n, DMAX>(a, hdr, pay_u32, empty, !last, xp, m, rsm, g, c, lane, frozen, refill)
+#define SC(n) sus_check<Q, KR, n, DMAX>(a, tinfo, hdr, pay_u32, empty, !last, xp, m, rsm, g, c, lane, frozen, refill)
         switch (d - 1) {
           case 0: SC(0); break;
           case 1: SC(1); break;
@@ -980,7 +1095,7 @@ __global__ void __launch_bounds__(SUSShape<Q, KR, DMAX, DVMAX, MARKOV, S, G>::TH
       if (last) {
         // vertical update of column j from the fresh r's (SUS step 2)
         group_bar<T>(g);  // rsm complete, transpose buffers free for the reduction
-#define SV(n) sus_vn<Q, KR, n, DVMAX, MARKOV, SS::PHASED && (T <= GFQ_ONEBAR_TMAX)>(a, hdr, xtra, Tp, empty, rsm, SS::PHASED ? stage_x : red, g, c, lane, frozen, SS::PHASED, refill)
+#define SV(n) sus_vn<Q, KR, n, DVMAX, MARKOV, SS::PHASED && (T <= GFQ_ONEBAR_TMAX)>(a, tinfo, hdr, xtra, Tp, empty, rsm, SS::PHASED ? stage_x : red, g, c, lane, frozen, SS::PHASED, refill)
         switch (dv) {
           case 0: SV(0); break;
           case 1: SV(1); break;
